@@ -1,0 +1,130 @@
+/*
+ * permb200.h — C ABI of the B200 permanent engine (libpermb200.so).
+ *
+ * The problem: given an N x N complex matrix A, return
+ *   Perm(A) = sum over permutations sigma of prod_i a_{i,sigma(i)}.
+ * Two evaluation formulas, both walked in Gray-code order on the GPU:
+ *   BB/FG (Glynn), Eq. (2), PAPER.md:66-68:
+ *     Perm(A) = 2^{-(N-1)} * sum_delta (prod_k delta_k) prod_i sum_j delta_j a_ij,
+ *     delta_1 = +1, delta_k in {-1,+1}; 2^{N-1} terms.
+ *   Ryser, Eq. (1), PAPER.md:62-64:
+ *     Perm(A) = (-1)^N sum_{S subset [N]} (-1)^{|S|} prod_i sum_{j in S} a_ij; 2^N terms.
+ *
+ * Index conventions (readings R2, R4, R5):
+ *   - a "Gray index" g ranges over [0, 2^{N-1}) (Glynn) or [0, 2^N) (Ryser); its code is
+ *     G(g) = g ^ (g >> 1).  Glynn: bit b of G set <=> delta_{b+2} = -1 (1-based), i.e.
+ *     column b+1 (0-based) carries a minus sign.  Ryser: bit b of G set <=> column b
+ *     (0-based) is in S.
+ *   - term(g) = sign(g) * prod_i rowsum_i(G(g)), sign = prod_k delta_k = (-1)^{popcount G}
+ *     (Glynn) or (-1)^{N - popcount G} (Ryser; the (-1)^N of Eq. (1) is folded per term).
+ *   - a "partial" is the UNSCALED sum of term(g) over a range of g, as complex
+ *     double-double.  The final factor 2^{-(N-1)} (Glynn) is applied exactly once, by
+ *     perm_combine / perm_glynn (PAPER.md:262-263 divides after ALLREDUCE; reading R3:
+ *     always, not only for odd N).
+ *
+ * Data layout: matrices are row-major n*n perm_c128 (interleaved re, im; identical to
+ * torch.complex128 / numpy complex128 / cuDoubleComplex).  Batches are `batch` such
+ * matrices back to back.
+ *
+ * Ownership and asynchrony: the CALLER owns every buffer.  Functions taking device
+ * pointers enqueue work on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ * default stream) on the CURRENT device and return immediately; outputs are valid after
+ * the stream is synchronised.  Temporary workspace is taken with cudaMallocAsync on
+ * `stream` and released on it.  Concurrent calls on different streams / devices are
+ * safe (the per-device constant-memory column slots are fenced with events).
+ * Functions suffixed _host take HOST pointers and are synchronous.
+ *
+ * Errors: every function returns PERM_OK (0) or an error code; nothing is written on
+ * PERM_EINVAL.  Asynchronous device faults surface at the caller's next synchronisation.
+ * Input VALUES are not checked: NaN / Inf propagate.  Results never contain -0.0.
+ */
+#ifndef PERMB200_H
+#define PERMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct { double re, im; } perm_c128;                          /* 16 B */
+typedef struct { double re_hi, re_lo, im_hi, im_lo; } perm_dd_c128;  /* 32 B */
+
+enum {
+  PERM_OK = 0,
+  PERM_EINVAL = 1,   /* null pointer, n < 1, n > perm_max_n(), batch < 0, lo > hi, hi > #terms, count < 1 */
+  PERM_ECUDA = 2,    /* CUDA runtime / launch error (message via perm_strerror(PERM_ECUDA)) */
+  PERM_ENOTIMPL = 3
+};
+
+enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1 };
+
+/* The canonical evaluation plan for (n, alg).  It depends only on (n, alg), never on
+ * the GPU count, so any partition of the unit range reproduces the single-GPU result
+ * bit for bit.
+ *   terms      = 2^log2_terms (2^{n-1} Glynn, 2^n Ryser)
+ *   chunk      = 2^chunk_bits consecutive Gray indices walked by one thread from a fresh
+ *                O(n^2) row-sum build (the drift reset)
+ *   leaf       = 2^leaf_bits chunks, walked in order by one thread into one dd accumulator
+ *   unit       = 2^block_bits leaves (one thread block) -> one dd partial
+ *   units      = 2^unit_bits; unit_terms = terms / units */
+typedef struct {
+  int n, alg;
+  int log2_terms, chunk_bits, leaf_bits, block_bits, unit_bits;
+  int reserved;
+  uint64_t unit_terms;
+  int64_t units;
+} perm_plan_t;
+
+/* Largest supported n (64).  n <= 56 keeps the row sums register-resident without
+ * spills; 57..64 are correct but slower (register spills). */
+int perm_max_n(void);
+
+/* Human-readable text for a status code (for PERM_ECUDA: the last CUDA error seen by
+ * this thread). */
+const char* perm_strerror(int code);
+
+/* Fill *plan for (n, alg).  PERM_EINVAL for bad n/alg or null plan. */
+int perm_plan(int n, int alg, perm_plan_t* plan);
+
+/* ---- single permanent (device pointers) -------------------------------------------- */
+/* out[0] = Perm(A) by Eq. (2) (perm_glynn) or Eq. (1) (perm_ryser).  A: device, n*n.
+ * out: device, 1 element.  = perm_sweep_units over all units + perm_combine. */
+int perm_glynn(const perm_c128* A, int n, perm_c128* out, void* stream);
+int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream);
+
+/* ---- building blocks for multi-GPU partitions --------------------------------------- */
+/* Sweep kernel only: unit partials for units [unit_lo, unit_hi) of plan(n, alg), written
+ * to unit_partials[0 .. unit_hi-unit_lo) (device).  One kernel launch (plus a tiny
+ * column-staging kernel).  Partials are unscaled. */
+int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_t unit_hi,
+                     perm_dd_c128* unit_partials, void* stream);
+
+/* Unscaled partial over Gray indices [lo, hi) (any lo <= hi <= #terms; ragged ends are
+ * walked by the library).  partial: device, 1 element.  If [lo, hi) is an aligned
+ * power-of-two block of units, the value equals that node of the canonical tree. */
+int perm_glynn_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream);
+int perm_ryser_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream);
+
+/* Canonical pairwise tree over `count` partials (device; zero-padded to a power of two:
+ * node = left + right in double-double, left = lower indices).  Writes the unscaled root
+ * to out_dd (device, may be NULL) and, if out (device) is not NULL, the final value:
+ * root * 2^{-(n-1)} (alg = GLYNN) or root (RYSER), rounded to complex128. */
+int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg,
+                 perm_c128* out, perm_dd_c128* out_dd, void* stream);
+
+/* ---- batched (device pointers): one permanent per thread block ---------------------- */
+/* out[b] = Perm(A_b) by Eq. (2), b < batch.  A: device, batch*n*n; out: device, batch.
+ * batch == 0 is a no-op returning PERM_OK. */
+int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream);
+
+/* ---- host-buffer entry points (synchronous; copies inside) -------------------------- */
+int perm_glynn_host(const perm_c128* A, int n, perm_c128* out);
+int perm_ryser_host(const perm_c128* A, int n, perm_c128* out);
+int perm_glynn_batched_host(const perm_c128* A, int n, int64_t batch, perm_c128* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PERMB200_H */

@@ -1,0 +1,161 @@
+"""paper_1606_05836_b200 — B200-native BB/FG (Glynn) and Ryser permanents.
+
+PAPER.md (arXiv 1606.05836): Eq. (2) BB/FG P:66-68 and Eq. (1) Ryser P:62-64, walked in
+Gray-code order by hand-written sm_100a FP64 kernels (paper_1606_05836_b200/csrc).  This
+module is the thin Python layer over the C ABI (include/permb200.h): it checks tensor
+shapes/dtypes/devices, passes raw device pointers and the current CUDA stream, and raises
+on any non-zero status.  PyTorch supplies device memory and streams only.
+
+    glynn(A) / ryser(A)              permanent of one n x n complex128 CUDA matrix
+    glynn_batched(As)                (B, n, n) -> (B,)  one permanent per thread block
+    glynn_range / ryser_range        unscaled double-double partial over Gray indices [lo, hi)
+    sweep_units / combine            the two kernels of the canonical reduction (multi-GPU)
+    glynn_host / ryser_host / glynn_batched_host   host-buffer C-ABI entry points
+    dist.perm_dist                   one permanent partitioned over a process group (NCCL)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import ALG_GLYNN, ALG_RYSER, Plan, PermError, max_n, plan  # noqa: F401
+
+__all__ = ["glynn", "ryser", "glynn_batched", "glynn_range", "ryser_range", "sweep_units", "combine",
+           "glynn_host", "ryser_host", "glynn_batched_host", "plan", "max_n", "Plan", "PermError",
+           "ALG_GLYNN", "ALG_RYSER"]
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _square(A: torch.Tensor) -> int:
+    if not isinstance(A, torch.Tensor) or A.dtype != torch.complex128 or not A.is_cuda:
+        raise TypeError("expected a torch.complex128 CUDA tensor")
+    if A.dim() != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError(f"expected a square matrix, got shape {tuple(A.shape)}")
+    return A.shape[0]
+
+
+def _alg(alg) -> int:
+    if alg in (ALG_GLYNN, "glynn"):
+        return ALG_GLYNN
+    if alg in (ALG_RYSER, "ryser"):
+        return ALG_RYSER
+    raise ValueError(f"unknown algorithm {alg!r}")
+
+
+def _perm(fn, name: str, A: torch.Tensor) -> torch.Tensor:
+    n = _square(A)
+    A = A.contiguous()
+    out = torch.empty((), dtype=torch.complex128, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(fn(A.data_ptr(), n, out.data_ptr(), _stream(A.device)), name)
+    return out
+
+
+def glynn(A: torch.Tensor) -> torch.Tensor:
+    """Perm(A) by BB/FG / Glynn, Eq. (2) (0-d complex128 tensor on A's device)."""
+    return _perm(_lib.lib().perm_glynn, "perm_glynn", A)
+
+
+def ryser(A: torch.Tensor) -> torch.Tensor:
+    """Perm(A) by Ryser, Eq. (1)."""
+    return _perm(_lib.lib().perm_ryser, "perm_ryser", A)
+
+
+def glynn_batched(As: torch.Tensor) -> torch.Tensor:
+    """(B, n, n) complex128 CUDA -> (B,) permanents, one thread block per matrix."""
+    if not isinstance(As, torch.Tensor) or As.dtype != torch.complex128 or not As.is_cuda:
+        raise TypeError("expected a torch.complex128 CUDA tensor")
+    if As.dim() != 3 or As.shape[1] != As.shape[2]:
+        raise ValueError(f"expected (B, n, n), got {tuple(As.shape)}")
+    B, n = As.shape[0], As.shape[1]
+    As = As.contiguous()
+    out = torch.empty((B,), dtype=torch.complex128, device=As.device)
+    with torch.cuda.device(As.device):
+        _lib.check(_lib.lib().perm_glynn_batched(As.data_ptr() if B else None, n, B, out.data_ptr() if B else None,
+                                                 _stream(As.device)), "perm_glynn_batched")
+    return out
+
+
+def _range(fn, name, A, lo, hi) -> torch.Tensor:
+    n = _square(A)
+    A = A.contiguous()
+    out = torch.empty(4, dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(fn(A.data_ptr(), n, int(lo), int(hi), out.data_ptr(), _stream(A.device)), name)
+    return out
+
+
+def glynn_range(A: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
+    """Unscaled Glynn partial over Gray indices [lo, hi) as (re_hi, re_lo, im_hi, im_lo) float64."""
+    return _range(_lib.lib().perm_glynn_range, "perm_glynn_range", A, lo, hi)
+
+
+def ryser_range(A: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
+    """Signed Ryser partial over Gray indices [lo, hi) (double-double, 4 float64)."""
+    return _range(_lib.lib().perm_ryser_range, "perm_ryser_range", A, lo, hi)
+
+
+def sweep_units(A: torch.Tensor, alg, unit_lo: int, unit_hi: int) -> torch.Tensor:
+    """Canonical unit partials for units [unit_lo, unit_hi) of plan(n, alg): (count, 4) float64."""
+    n = _square(A)
+    A = A.contiguous()
+    a = _alg(alg)
+    count = int(unit_hi) - int(unit_lo)
+    out = torch.empty((max(count, 0), 4), dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(_lib.lib().perm_sweep_units(A.data_ptr(), n, a, int(unit_lo), int(unit_hi),
+                                               out.data_ptr() if count > 0 else None, _stream(A.device)),
+                   "perm_sweep_units")
+    return out
+
+
+def combine(partials: torch.Tensor, n: int, alg, scale: bool = True):
+    """Canonical pairwise tree over (count, 4) float64 CUDA partials.  Returns (value, root_dd):
+    value = root * 2^-(n-1) (Glynn) rounded to complex128 if scale else None."""
+    if partials.dtype != torch.float64 or not partials.is_cuda or partials.dim() != 2 or partials.shape[1] != 4:
+        raise TypeError("expected a (count, 4) float64 CUDA tensor")
+    partials = partials.contiguous()
+    a = _alg(alg)
+    root = torch.empty(4, dtype=torch.float64, device=partials.device)
+    val = torch.empty((), dtype=torch.complex128, device=partials.device) if scale else None
+    with torch.cuda.device(partials.device):
+        _lib.check(_lib.lib().perm_combine(partials.data_ptr(), partials.shape[0], int(n), a,
+                                           val.data_ptr() if val is not None else None, root.data_ptr(),
+                                           _stream(partials.device)), "perm_combine")
+    return val, root
+
+
+def _host(fn, name, A, n, batch) -> "object":
+    import numpy as np
+    a = np.ascontiguousarray(A, dtype=np.complex128)
+    out = np.empty(1 if batch is None else max(batch, 1), dtype=np.complex128)
+    if batch is None:
+        _lib.check(fn(a.ctypes.data, n, out.ctypes.data), name)
+    else:
+        _lib.check(fn(a.ctypes.data, n, batch, out.ctypes.data), name)
+    return out
+
+
+def glynn_host(A) -> complex:
+    """Host-buffer entry point (C ABI perm_glynn_host): numpy in, complex out; copies inside."""
+    import numpy as np
+    a = np.ascontiguousarray(A, dtype=np.complex128)
+    return complex(_host(_lib.lib().perm_glynn_host, "perm_glynn_host", a, a.shape[0], None)[0])
+
+
+def ryser_host(A) -> complex:
+    import numpy as np
+    a = np.ascontiguousarray(A, dtype=np.complex128)
+    return complex(_host(_lib.lib().perm_ryser_host, "perm_ryser_host", a, a.shape[0], None)[0])
+
+
+def glynn_batched_host(As):
+    import numpy as np
+    a = np.ascontiguousarray(As, dtype=np.complex128)
+    B, n = a.shape[0], a.shape[1]
+    return _host(_lib.lib().perm_glynn_batched_host, "perm_glynn_batched_host", a, n, B)[:B]

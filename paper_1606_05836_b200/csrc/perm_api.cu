@@ -1,0 +1,343 @@
+// perm_api.cu — C ABI of libpermb200.so (declared in include/permb200.h): argument
+// checks, the canonical plan, constant-slot fencing, workspace, the combine kernel.
+//
+// PAPER.md: the per-process partial sums and the single ALLREDUCE followed by the final
+// division (Alg. A2) become: unit partials (sweep kernel) -> canonical
+// pairwise tree (combine kernel) -> x 2^-(n-1) exactly once (reading R3).
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/permb200.h"
+#include "perm_registry.h"
+
+using namespace permb200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return PERM_ECUDA;
+}
+
+#define CUDA_TRY(expr, where)                       \
+  do {                                              \
+    cudaError_t e_ = (expr);                        \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+struct DeviceSlots {
+  std::mutex mu;
+  bool init = false;
+  int next = 0;
+  cudaEvent_t ev[kSlots];
+  bool used[kSlots] = {};
+};
+DeviceSlots g_slots[64];
+
+std::once_flag g_tables_once;
+SweepLauncher g_sweep[2][kNMax + 1];
+BatchedLauncher g_batched[kNMax + 1];
+
+void init_tables() {
+  std::call_once(g_tables_once, [] {
+    register_glynn_a(g_sweep[kGlynn]);
+    register_glynn_b(g_sweep[kGlynn]);
+    register_glynn_c(g_sweep[kGlynn]);
+    register_glynn_d(g_sweep[kGlynn]);
+    register_ryser_a(g_sweep[kRyser]);
+    register_ryser_b(g_sweep[kRyser]);
+    register_ryser_c(g_sweep[kRyser]);
+    register_ryser_d(g_sweep[kRyser]);
+    register_batched_a(g_batched);
+    register_batched_b(g_batched);
+  });
+}
+
+int ceil_log2(long long v) {
+  int k = 0;
+  while ((1LL << k) < v) ++k;
+  return k;
+}
+
+void make_plan(int n, int alg, perm_plan_t* p) {
+  const int m = (alg == PERM_ALG_GLYNN) ? n - 1 : n;
+  int wbits, c, ubits, lam;
+  if (m < 5) {
+    wbits = 0; c = m; ubits = 0; lam = 0;      // tiny: one thread, generic walk
+  } else {
+    wbits = m - 5 < 7 ? m - 5 : 7;
+    const int rem = m - wbits;
+    int ct = ceil_log2(33LL * n);              // chunk build <= ~1% of the sweep's FP64 ops
+    if (ct < 5) ct = 5;
+    if (ct > kCMax) ct = kCMax;
+    const int ub_min = rem - 5 < 7 ? rem - 5 : 7;
+    c = rem - ub_min < ct ? rem - ub_min : ct;
+    if (c < 5) c = 5;
+    ubits = rem - c < 17 ? rem - c : 17;
+    lam = rem - c - ubits;
+  }
+  p->n = n; p->alg = alg;
+  p->log2_terms = m; p->chunk_bits = c; p->leaf_bits = lam; p->block_bits = wbits; p->unit_bits = ubits;
+  p->reserved = 0;
+  p->units = 1LL << ubits;
+  p->unit_terms = 1ULL << (m - ubits);
+}
+
+bool valid_n(int n) { return n >= 1 && n <= kNMax; }
+
+// Canonical tree over `count` partials (zero-padded to P = 2^k): one block of up to 1024
+// threads; thread t reduces the aligned segment [t*S, (t+1)*S) with the binary-counter
+// method (node = left + right), then a pairwise tree over the segment roots in smem.
+__global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int64_t P, int do_scale,
+                               int scale_exp, double2* out, Dd2* out_dd) {
+  __shared__ Dd2 red[1024];
+  const int64_t T = P < 1024 ? P : 1024;
+  const int64_t S = P / T;
+  const int tid = threadIdx.x;
+  if (tid < T) {
+    Dd2 stack[40];
+    int top_level = 0;
+    for (int64_t k = 0; k < S; ++k) {
+      const int64_t idx = tid * S + k;
+      Dd2 v = idx < count ? parts[idx] : Dd2{0.0, 0.0, 0.0, 0.0};
+      int lvl = 0;
+      for (int64_t kk = k; kk & 1; kk >>= 1) { v = dd2_add(stack[lvl], v); ++lvl; }
+      stack[lvl] = v;
+      if (lvl > top_level) top_level = lvl;
+    }
+    red[tid] = stack[top_level];
+  }
+  __syncthreads();
+  for (int64_t o = 1; o < T; o <<= 1) {
+    if ((tid & (2 * o - 1)) == 0 && tid + o < T) red[tid] = dd2_add(red[tid], red[tid + o]);
+    __syncthreads();
+  }
+  if (tid == 0) {
+    const Dd2 r = red[0];
+    if (out_dd) *out_dd = r;
+    if (out) {
+      const int e = do_scale ? scale_exp : 0;
+      double re = __dadd_rn(ldexp(r.re_hi, e), ldexp(r.re_lo, e));
+      double im = __dadd_rn(ldexp(r.im_hi, e), ldexp(r.im_lo, e));
+      if (re == 0.0) re = 0.0;   // canonical +0 (reading R11)
+      if (im == 0.0) im = 0.0;
+      *out = make_double2(re, im);
+    }
+  }
+}
+
+int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, Dd2* out_dd, cudaStream_t st) {
+  int64_t P = 1;
+  while (P < count) P <<= 1;
+  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, alg == PERM_ALG_GLYNN, -(n - 1), out, out_dd);
+  CUDA_TRY(cudaGetLastError(), "combine_kernel launch");
+  return PERM_OK;
+}
+
+// Sweep over units [u_lo, u_hi) clipped to Gray indices [lo, hi); partials -> out[0..).
+int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_hi, uint64_t lo, uint64_t hi,
+              Dd2* out, double2* staging, cudaStream_t st) {
+  init_tables();
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev), "cudaGetDevice");
+  if (dev < 0 || dev >= 64) { g_last_error = "device ordinal >= 64"; return PERM_ECUDA; }
+  SweepArgs a;
+  a.A = reinterpret_cast<const double2*>(A);
+  a.unit_out = out;
+  a.lo = lo; a.hi = hi;
+  a.unit_lo = u_lo;
+  a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
+  a.zero = 0;
+  DeviceSlots& ds = g_slots[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  if (!ds.init) {
+    for (int k = 0; k < kSlots; ++k) CUDA_TRY(cudaEventCreateWithFlags(&ds.ev[k], cudaEventDisableTiming), "cudaEventCreate");
+    ds.init = true;
+  }
+  const int slot = ds.next;
+  ds.next = (ds.next + 1) % kSlots;
+  // the constant slot may still be read by an earlier sweep on another stream: fence it
+  if (ds.used[slot]) CUDA_TRY(cudaStreamWaitEvent(st, ds.ev[slot], 0), "cudaStreamWaitEvent");
+  a.slot = slot;
+  a.col_base = slot * kTabRows * kNMax;
+  CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "sweep launch");
+  CUDA_TRY(cudaEventRecord(ds.ev[slot], st), "cudaEventRecord");
+  ds.used[slot] = true;
+  return PERM_OK;
+}
+
+constexpr size_t kStagingBytes = sizeof(double2) * kTabRows * kNMax;
+
+int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t st) {
+  if (!A || !out || !valid_n(n)) return PERM_EINVAL;
+  perm_plan_t P;
+  make_plan(n, alg, &P);
+  void* ws = nullptr;
+  const size_t bytes = kStagingBytes + sizeof(Dd2) * (size_t)P.units;
+  CUDA_TRY(cudaMallocAsync(&ws, bytes, st), "cudaMallocAsync");
+  double2* staging = static_cast<double2*>(ws);
+  Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
+  const uint64_t T = 1ULL << P.log2_terms;
+  int rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
+  if (rc == PERM_OK) rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), nullptr, st);
+  cudaError_t e = cudaFreeAsync(ws, st);
+  if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return rc;
+}
+
+int range_perm(const perm_c128* A, int n, int alg, uint64_t lo, uint64_t hi, perm_dd_c128* partial, cudaStream_t st) {
+  if (!A || !partial || !valid_n(n)) return PERM_EINVAL;
+  perm_plan_t P;
+  make_plan(n, alg, &P);
+  const uint64_t T = 1ULL << P.log2_terms;
+  if (lo > hi || hi > T) return PERM_EINVAL;
+  if (lo == hi) {
+    CUDA_TRY(cudaMemsetAsync(partial, 0, sizeof(perm_dd_c128), st), "cudaMemsetAsync");
+    return PERM_OK;
+  }
+  const int64_t u_lo = (int64_t)(lo / P.unit_terms);
+  const int64_t u_hi = (int64_t)((hi + P.unit_terms - 1) / P.unit_terms);
+  void* ws = nullptr;
+  const size_t bytes = kStagingBytes + sizeof(Dd2) * (size_t)(u_hi - u_lo);
+  CUDA_TRY(cudaMallocAsync(&ws, bytes, st), "cudaMallocAsync");
+  double2* staging = static_cast<double2*>(ws);
+  Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
+  int rc = run_sweep(A, P, u_lo, u_hi, lo, hi, parts, staging, st);
+  if (rc == PERM_OK) rc = run_combine(parts, u_hi - u_lo, n, alg, nullptr, reinterpret_cast<Dd2*>(partial), st);
+  cudaError_t e = cudaFreeAsync(ws, st);
+  if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return rc;
+}
+
+void make_batched_plan(int n, int* block_bits, int* c, int* lam) {
+  const int m = n - 1;
+  if (m < 5) { *block_bits = 0; *c = m; *lam = 0; return; }
+  int wb = m - 5 < 7 ? m - 5 : 7;
+  const int rem = m - wb;
+  int cc = rem < kCMax ? rem : kCMax;
+  *block_bits = wb; *c = cc; *lam = rem - cc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int perm_max_n(void) { return kNMax; }
+
+const char* perm_strerror(int code) {
+  switch (code) {
+    case PERM_OK: return "ok";
+    case PERM_EINVAL: return "invalid argument";
+    case PERM_ECUDA: return g_last_error.empty() ? "CUDA error" : g_last_error.c_str();
+    case PERM_ENOTIMPL: return "not implemented";
+    default: return "unknown status";
+  }
+}
+
+int perm_plan(int n, int alg, perm_plan_t* plan) {
+  if (!plan || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  make_plan(n, alg, plan);
+  return PERM_OK;
+}
+
+int perm_glynn(const perm_c128* A, int n, perm_c128* out, void* stream) {
+  return full_perm(A, n, PERM_ALG_GLYNN, out, static_cast<cudaStream_t>(stream));
+}
+
+int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream) {
+  return full_perm(A, n, PERM_ALG_RYSER, out, static_cast<cudaStream_t>(stream));
+}
+
+int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_t unit_hi,
+                     perm_dd_c128* unit_partials, void* stream) {
+  if (!A || !unit_partials || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  perm_plan_t P;
+  make_plan(n, alg, &P);
+  if (unit_lo < 0 || unit_lo > unit_hi || unit_hi > P.units) return PERM_EINVAL;
+  if (unit_lo == unit_hi) return PERM_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, kStagingBytes, st), "cudaMallocAsync");
+  const uint64_t lo = (uint64_t)unit_lo * P.unit_terms, hi = (uint64_t)unit_hi * P.unit_terms;
+  int rc = run_sweep(A, P, unit_lo, unit_hi, lo, hi, reinterpret_cast<Dd2*>(unit_partials), static_cast<double2*>(ws), st);
+  cudaError_t e = cudaFreeAsync(ws, st);
+  if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return rc;
+}
+
+int perm_glynn_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream) {
+  return range_perm(A, n, PERM_ALG_GLYNN, lo, hi, partial, static_cast<cudaStream_t>(stream));
+}
+
+int perm_ryser_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream) {
+  return range_perm(A, n, PERM_ALG_RYSER, lo, hi, partial, static_cast<cudaStream_t>(stream));
+}
+
+int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg, perm_c128* out,
+                 perm_dd_c128* out_dd, void* stream) {
+  if (!partials || count < 1 || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  if (!out && !out_dd) return PERM_EINVAL;
+  return run_combine(reinterpret_cast<const Dd2*>(partials), count, n, alg, reinterpret_cast<double2*>(out),
+                     reinterpret_cast<Dd2*>(out_dd), static_cast<cudaStream_t>(stream));
+}
+
+int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream) {
+  if (!valid_n(n) || batch < 0) return PERM_EINVAL;
+  if (batch == 0) return PERM_OK;
+  if (!A || !out) return PERM_EINVAL;
+  init_tables();
+  BatchedArgs a;
+  a.A = reinterpret_cast<const double2*>(A);
+  a.out = reinterpret_cast<double2*>(out);
+  a.batch = batch;
+  make_batched_plan(n, &a.block_bits, &a.c, &a.lam);
+  a.scale_exp = -(n - 1);
+  a.zero = 0;
+  const int grid = batch < (1LL << 30) ? (int)batch : (1 << 30);
+  CUDA_TRY(g_batched[n](a, grid, static_cast<cudaStream_t>(stream)), "batched launch");
+  return PERM_OK;
+}
+
+static int host_call(const perm_c128* A, int n, int64_t batch, perm_c128* out, int which) {
+  if (!A || !out || !valid_n(n) || batch < 0) return PERM_EINVAL;
+  if (batch == 0) return PERM_OK;
+  cudaStream_t st = nullptr;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+  void* dA = nullptr;
+  void* dO = nullptr;
+  const size_t abytes = sizeof(perm_c128) * (size_t)n * n * batch, obytes = sizeof(perm_c128) * batch;
+  int rc = PERM_OK;
+  cudaError_t e = cudaMallocAsync(&dA, abytes, st);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dO, obytes, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "host entry: alloc/copy in");
+  if (rc == PERM_OK) {
+    const perm_c128* a = static_cast<const perm_c128*>(dA);
+    perm_c128* o = static_cast<perm_c128*>(dO);
+    if (which == 0) rc = perm_glynn(a, n, o, st);
+    else if (which == 1) rc = perm_ryser(a, n, o, st);
+    else rc = perm_glynn_batched(a, n, batch, o, st);
+  }
+  if (rc == PERM_OK) {
+    e = cudaMemcpyAsync(out, dO, obytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host entry: copy out");
+  }
+  if (dA) cudaFreeAsync(dA, st);
+  if (dO) cudaFreeAsync(dO, st);
+  e = cudaStreamSynchronize(st);
+  if (rc == PERM_OK && e != cudaSuccess) rc = cuda_fail(e, "host entry: synchronize");
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+int perm_glynn_host(const perm_c128* A, int n, perm_c128* out) { return host_call(A, n, 1, out, 0); }
+int perm_ryser_host(const perm_c128* A, int n, perm_c128* out) { return host_call(A, n, 1, out, 1); }
+int perm_glynn_batched_host(const perm_c128* A, int n, int64_t batch, perm_c128* out) {
+  return host_call(A, n, batch, out, 2);
+}
+
+}  // extern "C"

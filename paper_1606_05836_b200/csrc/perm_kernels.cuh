@@ -1,0 +1,478 @@
+// perm_kernels.cuh — sm_100a FP64 Gray-code sweep kernels for Glynn (BB/FG, Eq. 2) and
+// Ryser (Eq. 1) permanents.  Included only by the perm_inst_*.cu translation units, each
+// of which instantiates a range of n (one template instantiation per n keeps the n
+// complex row sums register-resident: DESIGN.md §Kernels).
+//
+// PAPER.md citations ("P:<line>"):
+//   Eq. (2) P:66-68  perm = 2^-(N-1) sum_delta (prod delta_k) prod_i sum_j delta_j a_ij
+//   Eq. (1) P:62-64  perm = (-1)^N sum_S (-1)^|S| prod_i sum_{j in S} a_ij
+//   Alg. A2 loop body P:251-260 (delta decode, row sums, product, signed accumulate)
+//   Alg. A1 loop body P:220-229
+//   per-process partial + one ALLREDUCE
+//
+// What differs from the paper's loop ("O(2^N N^2)"): consecutive terms are visited in
+// Gray-code order so each term costs ONE +-2*column (Glynn) / +-column (Ryser) update of
+// the n row sums plus one n-way complex product: O(n) per term (north_star).
+//
+// Structure of one thread's work:
+//   leaf  = 2^lam chunks, walked in order, one compensated accumulator;
+//   chunk = 2^c Gray indices: O(n^2) row-sum build from the code (drift reset), then two
+//           half-walks of 2^(c-1) steps separated by the one flip whose direction is
+//           per-thread (Gray bit c-1 flips with direction = bit c of g = bit 0 of q);
+//   in a half-walk every thread flips the SAME column b = ctz(t) with the SAME direction
+//   at the same step, so the column is a warp-uniform operand: it is read from the
+//   constant bank with a uniform index (LDCU -> uniform register -> DFMA operand), which
+//   costs no vector register and no shared-memory bandwidth.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace permb200 {
+
+enum { kGlynn = 0, kRyser = 1 };
+
+constexpr int kNMax = 64;      // largest n
+constexpr int kCMax = 12;      // largest chunk_bits
+constexpr int kTabRows = 16;   // rows per constant slot; rows >= c (incl. 15) are zero
+constexpr int kSlots = 3;      // constant-memory column slots per translation unit (3 x 16 KB)
+constexpr int kMaxBlock = 128; // threads per block (block_bits <= 7)
+
+struct Dd2 { double re_hi, re_lo, im_hi, im_lo; };
+
+// Arguments of one sweep launch (plain struct, passed by value).
+struct SweepArgs {
+  const double2* A;      // device, row-major n*n
+  Dd2* unit_out;         // device, one partial per launched unit (blockIdx.x)
+  uint64_t lo, hi;       // clip range of Gray indices
+  int64_t unit_lo;       // global index of the unit run by blockIdx.x == 0
+  int c, lam, block_bits;
+  int slot;              // constant-memory column slot
+  int col_base;          // slot * kTabRows * kNMax, precomputed on the host: an index formed by
+                         // multiplying in the kernel defeats ptxas' uniform-register path
+  int zero;              // always 0; opaque to the compiler (keeps column loads in the loop)
+};
+
+struct BatchedArgs {
+  const double2* A;      // device, batch * n*n
+  double2* out;          // device, batch
+  int64_t batch;
+  int c, lam, block_bits;
+  int scale_exp;         // -(n-1)
+  int zero;
+};
+
+// ------------------------------------------------------------------ FP64 building blocks
+// All rounding steps are explicit (__dadd_rn / __dmul_rn / __fma_rn) so --fmad cannot
+// change them (reading R6).
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  double2 r;
+  r.x = __fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y));
+  r.y = __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x));
+  return r;
+}
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+
+__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  e = __dsub_rn(b, __dsub_rn(s, a));
+}
+
+// double-double + double-double (accurate variant); result normalised.
+__device__ __forceinline__ void dd_add(double ah, double al, double bh, double bl, double& rh, double& rl) {
+  double s, e, t, f;
+  two_sum(ah, bh, s, e);
+  two_sum(al, bl, t, f);
+  e = __dadd_rn(e, t);
+  fast_two_sum(s, e, s, e);
+  e = __dadd_rn(e, f);
+  fast_two_sum(s, e, rh, rl);
+}
+
+__device__ __forceinline__ Dd2 dd2_add(const Dd2& a, const Dd2& b) {
+  Dd2 r;
+  dd_add(a.re_hi, a.re_lo, b.re_hi, b.re_lo, r.re_hi, r.re_lo);
+  dd_add(a.im_hi, a.im_lo, b.im_hi, b.im_lo, r.im_hi, r.im_lo);
+  return r;
+}
+
+// Product of the n row sums: 4 independent chains (i mod 4) then a pairwise tree.
+// The order depends only on N, so every kernel/launch shape computes identical terms.
+template <int N>
+__device__ __forceinline__ double2 row_product(const double2 (&s)[N]) {
+  constexpr int NC = N < 4 ? N : 4;
+  double2 c[NC];
+#pragma unroll
+  for (int k = 0; k < NC; ++k) c[k] = s[k];
+#pragma unroll
+  for (int i = NC; i < N; ++i) c[i % NC] = cmul(c[i % NC], s[i]);
+#pragma unroll
+  for (int w = 1; w < NC; w *= 2) {
+#pragma unroll
+    for (int k = 0; k + w < NC; k += 2 * w) c[k] = cmul(c[k], c[k + w]);
+  }
+  return c[0];
+}
+
+// ------------------------------------------------------------------ column sources
+// Flip of Gray bit b touches matrix column col0 + b (Glynn col0 = 1: bit b <-> delta_{b+2};
+// Ryser col0 = 0: bit b <-> column b).
+//
+// ConstColumns: table[slot][b][i] = kScale * a_{i, col0+b} for b < c, zero for c <= b < 16.
+// Declared per translation unit (static): each TU stages its own copy.
+static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
+
+struct ConstColumns {
+  int base;
+  __device__ __forceinline__ double2 get(int b, int i) const { return c_cols[base + b * kNMax + i]; }
+};
+
+// SmemColumns: a per-block shared-memory table with the same layout as the constant one:
+// tab[b*N + i] = step vector of Gray bit b for b < c, zero for c <= b < 16.
+template <int N>
+struct SmemColumns {
+  const double2* tab;
+  __device__ __forceinline__ double2 get(int b, int i) const { return tab[b * N + i]; }
+};
+
+// ------------------------------------------------------------------ the walker
+template <int N, int ALG>
+struct Walker {
+  double2 s[N];                  // row sums (registers)
+  double arh, arl, aih, ail;     // cascaded (Sum2) double-double accumulators
+
+  // Column sources hold STEP VECTORS u = kScale * column (Glynn 2a: exact doubling; Ryser a).
+  // Direction bit d of a flip: Glynn d=1 -> delta back to +1 -> +u, d=0 -> delta to -1 -> -u;
+  // Ryser d=1 -> column leaves S -> -u, d=0 -> joins S -> +u.
+  static constexpr double kScale = (ALG == kGlynn) ? 2.0 : 1.0;
+  static constexpr double kSgnDir1 = (ALG == kGlynn) ? 1.0 : -1.0;
+  static constexpr double kSgnDir0 = (ALG == kGlynn) ? -1.0 : 1.0;
+  // term sign base: Glynn (-1)^g ; Ryser (-1)^(N+g)
+  static constexpr bool kNegBase = (ALG == kRyser) && (N & 1);
+
+  __device__ __forceinline__ void zero_acc() { arh = arl = aih = ail = 0.0; }
+
+  __device__ __forceinline__ void acc_add(double re, double im) {
+    double s_, e_;
+    two_sum(arh, re, s_, e_);
+    arh = s_; arl = __dadd_rn(arl, e_);
+    two_sum(aih, im, s_, e_);
+    aih = s_; ail = __dadd_rn(ail, e_);
+  }
+
+  // Chunk-start row sums for code G ("Convert iter to the set delta ...
+  // Calculate s"), O(n^2), from the transposed, pre-scaled matrix in shared memory.  Rows are done
+  // 8 at a time with a runtime column loop, which bounds the registers the loads take.
+  __device__ __forceinline__ void build(const double2* __restrict__ at, uint64_t G) {
+    constexpr int RB = 8;
+#pragma unroll
+    for (int r0 = 0; r0 < N; r0 += RB) {
+#pragma unroll
+      for (int i = r0; i < r0 + RB; ++i)
+        if (i < N) {
+          if (ALG == kGlynn) s[i] = make_double2(0.5 * at[i].x, 0.5 * at[i].y);  // delta_1 = +1; exact
+          else s[i] = make_double2(0.0, 0.0);          // Ryser: S starts empty
+        }
+#pragma unroll 1
+      for (int j = (ALG == kGlynn) ? 1 : 0; j < N; ++j) {
+        const int bit = (ALG == kGlynn) ? (int)((G >> (j - 1)) & 1) : (int)((G >> j) & 1);
+        // at holds kScale * a: weight delta_j / 2 (Glynn) reproduces RN(s + delta_j a_ij) exactly
+        const double w = (ALG == kGlynn) ? (bit ? -0.5 : 0.5) : (bit ? 1.0 : 0.0);
+        const double2* col = at + j * N;
+#pragma unroll
+        for (int i = r0; i < r0 + RB; ++i)
+          if (i < N) {
+            const double2 v = col[i];
+            s[i].x = __fma_rn(w, v.x, s[i].x);
+            s[i].y = __fma_rn(w, v.y, s[i].y);
+          }
+      }
+    }
+  }
+
+  // s_i <- s_i + sg * u_b,i with a runtime sign sg in {-1, 0, +1}: one DFMA per real
+  // component; the step vector is the uniform operand (UR), sg a vector register.
+  template <class Cols>
+  __device__ __forceinline__ void flip(const Cols& cols, int b, double sg) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double2 v = cols.get(b, i);
+      s[i].x = __fma_rn(sg, v.x, s[i].x);
+      s[i].y = __fma_rn(sg, v.y, s[i].y);
+    }
+  }
+  // Uniform half-walk.  State on entry = row sums at local index T0; visits local indices
+  // T0 .. T0+H-1 (H = 2^(c-1) >= 16).  Iteration t (t = -4, 0, 4, ..., H-8) visits
+  // T0+t+4 .. T0+t+7:  r=0 flips Gray bit b = ctz(t+4) (t = -4: table row 15, all zeros:
+  // no flip), r=1 bit 0, r=2 bit 1, r=3 bit 0.  Direction of the flip into index g is
+  // bit (b+1) of g, so r=1 -> 0, r=3 -> 1, r=2 -> bit 2 of t+4 and r=0
+  // -> bit b+1 of T0+t+4: all warp-uniform.  Terms alternate in sign (parity of G(g) =
+  // parity of g); plain sums over 16 terms, then the compensated (Sum2) accumulator.
+  //
+  // The loop is written in exactly this shape on purpose: one flip call site per unrolled
+  // step with (b, sg) selected by r, and the opaque tz = t*zero in the compile-time
+  // column indices.  ptxas then keeps t in a uniform register and reads the columns with
+  // LDCU (uniform operand, no vector register); other spellings of the same loop made it
+  // fall back to per-thread LDC + spills (tests/test_build_sass.py guards this).
+  template <class Cols>
+  __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero) {
+    double mr = 0.0, mi = 0.0;
+    for (int t = -4; t < H - 4; t += 4) {
+      const int tz = t * zero;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1) + tz;
+        const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
+        const double sg = d ? kSgnDir1 : kSgnDir0;
+        flip(cols, b, sg);
+        const double2 p = row_product<N>(s);
+        if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
+        else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
+      }
+      if (((t + 4) & 12) == 12) { acc_add(mr, mi); mr = 0.0; mi = 0.0; }
+    }
+    acc_add(mr, mi);
+  }
+
+  // Full aligned chunk q (Gray indices [q 2^c, (q+1) 2^c)), c >= 5.
+  template <class Cols>
+  __device__ __forceinline__ void fast_chunk(const Cols& cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
+    const uint64_t g0 = q << c;
+    build(at, g0 ^ (g0 >> 1));
+    const int H = 1 << (c - 1);
+    half_walk(cols, 0, H, zero);
+    flip(cols, c - 1, (q & 1) ? kSgnDir1 : kSgnDir0);   // direction = bit c of g = bit 0 of q
+    half_walk(cols, H, H, zero);
+  }
+
+  // Generic walk over [ga, gb) inside one aligned chunk (ragged range ends, tiny n):
+  // per-thread columns from shared memory, per-term compensated accumulation.
+  __device__ __forceinline__ void generic_walk(const double2* __restrict__ at, uint64_t ga, uint64_t gb) {
+    constexpr int col0 = (ALG == kGlynn) ? 1 : 0;
+    build(at, ga ^ (ga >> 1));
+    for (uint64_t g = ga;; ) {
+      double2 p = row_product<N>(s);
+      const bool neg = ((g & 1) != 0) != kNegBase;
+      if (neg) { p.x = -p.x; p.y = -p.y; }
+      acc_add(p.x, p.y);
+      if (++g >= gb) break;
+      const int b = __ffsll((long long)g) - 1;
+      const double sg = ((g >> (b + 1)) & 1) ? kSgnDir1 : kSgnDir0;
+      const double2* col = at + (col0 + b) * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double2 v = col[i];
+        s[i].x = __fma_rn(sg, v.x, s[i].x);
+        s[i].y = __fma_rn(sg, v.y, s[i].y);
+      }
+    }
+  }
+
+  __device__ __forceinline__ Dd2 result() const {
+    Dd2 r;
+    fast_two_sum(arh, arl, r.re_hi, r.re_lo);
+    fast_two_sum(aih, ail, r.im_hi, r.im_lo);
+    return r;
+  }
+};
+
+// One full aligned chunk q, c >= 5, as its own (non-inlined) function.  Keeping the walk
+// in a separate ptxas allocation unit is what lets ptxas hold the half-walk loop counter in
+// a uniform register and feed the column operands from LDCU; inlined into the leaf loop
+// (a loop nest with the build's loop) it fell back to per-thread LDC and spilled.
+template <int N, int ALG, class Cols>
+__device__ __noinline__ Dd2 chunk_fast(const Cols cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
+  Walker<N, ALG> w;
+  w.zero_acc();
+  w.fast_chunk(cols, at, q, c, zero);
+  return w.result();
+}
+
+// Ragged piece [ga, gb) of one chunk (range ends, tiny n).
+template <int N, int ALG>
+__device__ __noinline__ Dd2 chunk_generic(const double2* __restrict__ at, uint64_t ga, uint64_t gb) {
+  Walker<N, ALG> w;
+  w.zero_acc();
+  w.generic_walk(at, ga, gb);
+  return w.result();
+}
+
+// One leaf = 2^lam consecutive chunks walked in order by one thread; chunk partials are
+// combined in order with double-double additions.  kFast: every chunk lies inside the
+// range and c >= 5 (decided by the caller from block-uniform values).
+template <int N, int ALG, bool kFast, class Cols>
+__device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
+                                         int c, int lam, uint64_t lo, uint64_t hi, int zero) {
+  Dd2 acc{0.0, 0.0, 0.0, 0.0};
+  const uint64_t nchunks = 1ull << lam;
+  for (uint64_t k = 0; k < nchunks; ++k) {
+    const uint64_t q = (leaf_id << lam) + k;
+    if (kFast) {
+      acc = dd2_add(acc, chunk_fast<N, ALG>(cols, at, q, c, zero));
+    } else {
+      const uint64_t g0 = q << c, g1 = g0 + (1ull << c);
+      const uint64_t ga = g0 > lo ? g0 : lo;
+      const uint64_t gb = g1 < hi ? g1 : hi;
+      if (ga < gb) acc = dd2_add(acc, chunk_generic<N, ALG>(at, ga, gb));
+    }
+  }
+  return acc;
+}
+
+// Transposed, pre-scaled copy of one n*n row-major matrix into shared memory:
+// at[j*N + i] = scale * a_ij (scale 2 for Glynn, exact; 1 for Ryser).
+template <int N>
+__device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, double2* at, double scale) {
+  for (int k = threadIdx.x; k < N * N; k += blockDim.x) {
+    const int i = k / N, j = k - i * N;
+    double2 v = A[k];
+    v.x *= scale;
+    v.y *= scale;
+    at[j * N + i] = v;
+  }
+}
+
+// Canonical block reduction: contiguous pairwise tree over the block's threads (leaves),
+// node = left + right in double-double.  Result valid in red[0].
+__device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  red[tid] = mine;
+  __syncthreads();
+  for (int o = 1; o < nt; o <<= 1) {
+    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = dd2_add(red[tid], red[tid + o]);
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+// One block = one unit of the canonical plan.  Dynamic shared memory: N*N double2
+// (transposed matrix) + blockDim Dd2 (reduction).
+template <int N, int ALG>
+__global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) {
+  extern __shared__ double2 smem[];
+  double2* at = smem;
+  Dd2* red = reinterpret_cast<Dd2*>(smem + N * N);
+  stage_transposed<N>(args.A, at, Walker<N, ALG>::kScale);
+  __syncthreads();
+
+  const ConstColumns cols{args.col_base};
+  const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
+  const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
+  const int ubits = args.block_bits + args.lam + args.c;          // log2(unit terms)
+  const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
+  Dd2 mine;
+  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+
+  block_tree(red, mine);
+  if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
+}
+
+// Batched Glynn: block b computes Perm(A_b) completely (boson sampling needs
+// many permanents of n x n submatrices).  Columns come from the block's shared-memory copy
+// (warp-uniform addresses: broadcast LDS).
+template <int N>
+__global__ void __launch_bounds__(kMaxBlock) batched_kernel(const BatchedArgs args) {
+  extern __shared__ double2 smem[];
+  double2* at = smem;
+  double2* tab = smem + N * N;
+  Dd2* red = reinterpret_cast<Dd2*>(smem + N * N + kTabRows * N);
+  for (int64_t b = blockIdx.x; b < args.batch; b += gridDim.x) {
+    __syncthreads();
+    stage_transposed<N>(args.A + b * (int64_t)(N * N), at, 2.0);
+    __syncthreads();
+    for (int k = threadIdx.x; k < kTabRows * N; k += blockDim.x) {
+      const int bb = k / N, i = k - bb * N;
+      tab[k] = (bb < args.c && 1 + bb < N) ? at[(1 + bb) * N + i] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const SmemColumns<N> cols{tab};
+    const uint64_t terms = 1ull << (N - 1);
+    Dd2 mine;
+    if (args.c >= 5) mine = walk_leaf<N, kGlynn, true>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
+    else mine = walk_leaf<N, kGlynn, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
+    block_tree(red, mine);
+    if (threadIdx.x == 0) {
+      const Dd2 r = red[0];
+      double re = __dadd_rn(ldexp(r.re_hi, args.scale_exp), ldexp(r.re_lo, args.scale_exp));
+      double im = __dadd_rn(ldexp(r.im_hi, args.scale_exp), ldexp(r.im_lo, args.scale_exp));
+      if (re == 0.0) re = 0.0;   // canonical +0
+      if (im == 0.0) im = 0.0;
+      args.out[b] = make_double2(re, im);
+    }
+  }
+}
+
+// Column staging: table[b][i] = a_{i, col0+b}, b < c  (written to a device buffer, then
+// copied into this TU's constant slot with cudaMemcpyToSymbolAsync).
+static __global__ void stage_columns_kernel(const double2* __restrict__ A, int n, int col0, int c, double scale,
+                                     double2* table) {
+  for (int k = threadIdx.x; k < kTabRows * kNMax; k += blockDim.x) {
+    const int b = k / kNMax, i = k - b * kNMax;
+    double2 v = make_double2(0.0, 0.0);
+    if (b < c && i < n && col0 + b < n) {
+      v = A[(size_t)i * n + col0 + b];
+      v.x *= scale;   // x2 is exact
+      v.y *= scale;
+    }
+    table[k] = v;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+using SweepLauncher = cudaError_t (*)(const SweepArgs&, int64_t units, double2* staging, cudaStream_t);
+using BatchedLauncher = cudaError_t (*)(const BatchedArgs&, int grid, cudaStream_t);
+
+template <int N, int ALG>
+cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cudaStream_t st) {
+  const int c_tab = a.c < kCMax ? a.c : kCMax;
+  const int col0 = (ALG == kGlynn) ? 1 : 0;
+  if (a.c >= 5) {
+    stage_columns_kernel<<<1, 256, 0, st>>>(a.A, N, col0, c_tab, (ALG == kGlynn) ? 2.0 : 1.0, staging);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyToSymbolAsync(c_cols, staging, sizeof(double2) * kTabRows * kNMax,
+                                sizeof(double2) * (size_t)a.slot * kTabRows * kNMax, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return e;
+  }
+  const int threads = 1 << a.block_bits;
+  const size_t smem = sizeof(double2) * N * N + sizeof(Dd2) * threads;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  sweep_kernel<N, ALG><<<(unsigned)units, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int N>
+cudaError_t launch_batched(const BatchedArgs& a, int grid, cudaStream_t st) {
+  const int threads = 1 << a.block_bits;
+  const size_t smem = sizeof(double2) * (N * N + kTabRows * N) + sizeof(Dd2) * threads;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(batched_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  batched_kernel<N><<<grid, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace permb200
+
+// Instantiate launchers for n in [LO, HI] of algorithm ALG and register them in a table.
+#include <utility>
+namespace permb200 {
+template <int ALG, int LO, int... Is>
+void fill_sweep(SweepLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG>), ...);
+}
+template <int LO, int... Is>
+void fill_batched(BatchedLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_batched<LO + Is>), ...);
+}
+}  // namespace permb200

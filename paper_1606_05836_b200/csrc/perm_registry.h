@@ -1,0 +1,16 @@
+// perm_registry.h — per-translation-unit launcher registration (one template instance per n).
+#pragma once
+#include "perm_kernels.cuh"
+
+namespace permb200 {
+void register_glynn_a(SweepLauncher* t);
+void register_glynn_b(SweepLauncher* t);
+void register_glynn_c(SweepLauncher* t);
+void register_glynn_d(SweepLauncher* t);
+void register_ryser_a(SweepLauncher* t);
+void register_ryser_b(SweepLauncher* t);
+void register_ryser_c(SweepLauncher* t);
+void register_ryser_d(SweepLauncher* t);
+void register_batched_a(BatchedLauncher* t);
+void register_batched_b(BatchedLauncher* t);
+}  // namespace permb200

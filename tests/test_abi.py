@@ -1,0 +1,71 @@
+"""CPU-side checks of the C-ABI library (no GPU needed): it loads, exports every symbol the
+header declares, validates arguments before touching CUDA, and plans canonically."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1606_05836_b200 as pb
+from paper_1606_05836_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "permb200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(perm_\w+)\s*\(", text, re.M)))
+
+
+def test_library_loads_and_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = _declared()
+    assert len(declared) >= 13
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(declared) == set(_lib.EXPORTS)
+
+
+def test_max_n_and_strerror():
+    assert pb.max_n() == 64
+    assert _lib.strerror(0) == "ok"
+    assert "invalid" in _lib.strerror(1)
+    assert _lib.strerror(3) == "not implemented"
+
+
+def test_invalid_arguments_rejected_without_cuda():
+    L = _lib.lib()
+    buf = ctypes.create_string_buffer(64)
+    assert L.perm_glynn(None, 4, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_glynn(buf, 0, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_ryser(buf, 65, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_glynn_batched(buf, 4, -1, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_glynn_batched(None, 4, 0, None, None) == _lib.PERM_OK     # empty batch: no-op
+    assert L.perm_glynn_range(buf, 4, 5, 4, buf, None) == _lib.PERM_EINVAL   # lo > hi
+    assert L.perm_glynn_range(buf, 4, 0, 9, buf, None) == _lib.PERM_EINVAL   # hi > 2^(n-1)
+    assert L.perm_sweep_units(buf, 4, 2, 0, 1, buf, None) == _lib.PERM_EINVAL  # bad alg
+    assert L.perm_combine(buf, 0, 4, 0, buf, buf, None) == _lib.PERM_EINVAL   # count < 1
+    assert L.perm_glynn_host(None, 3, buf) == _lib.PERM_EINVAL
+    with pytest.raises(pb.PermError):
+        pb.plan(0)
+
+
+@pytest.mark.parametrize("alg", [pb.ALG_GLYNN, pb.ALG_RYSER])
+def test_plan_is_a_partition(alg):
+    for n in range(1, 65):
+        P = pb.plan(n, alg)
+        m = n - 1 if alg == pb.ALG_GLYNN else n
+        assert P.log2_terms == m
+        assert P.chunk_bits + P.leaf_bits + P.block_bits + P.unit_bits == m
+        assert P.units * P.unit_terms == 1 << m
+        assert 0 <= P.block_bits <= 7 and 0 <= P.chunk_bits <= 12
+        if m >= 5:
+            assert P.chunk_bits >= 5                       # fast path usable
+        assert P.units <= 1 << 17
+
+
+def test_plan_large_n_shards_eight_ways():
+    for n in (32, 40, 50):
+        P = pb.plan(n)
+        assert P.units % 8 == 0 and P.units >= 4096

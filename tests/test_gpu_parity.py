@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on the same seeded inputs (task rule ③).  Tolerance classes from SURVEY §8(c) / DESIGN.md:
+
+  E  bit-exact: integer matrices meeting the exactness precondition (oracle.exact(...)
+     .fp64_exact_eligible(): every partial product and partial sum an integer < 2^53)
+  R  relative <= 1e-9 vs the double-double oracle (north_star), Gaussian / Haar, n <= 28
+  B  |gpu - oracle| <= (n + 2^(c/2)) * u * L1 (walk-aware, L1 = sum |term| from the oracle);
+     Ryser passes with R or B (the paper's finding: FP64 Ryser cannot meet 1e-9)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_1606_05836_b200 as pb
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+U = 2.0 ** -53
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).to(DEV)
+
+
+def cval(t) -> complex:
+    return complex(t.item())
+
+
+def dd_to_complex(t) -> complex:
+    v = t.cpu().numpy()
+    return complex(v[0] + v[1], v[2] + v[3])
+
+
+# ----------------------------------------------------------------- class E (bit-exact)
+def _e_cases():
+    cases = [("2x2", np.array([[1, 2], [3, 4]]))]
+    for n in (1, 2, 3, 5, 8, 11, 12, 13):
+        cases.append((f"J{n}", synth.ones(n)))
+        cases.append((f"J-I{n}", synth.ones_minus_eye(n)))
+    for n in (1, 6, 17, 24):
+        cases.append((f"I{n}", synth.eye(n)))
+        p = np.random.default_rng(n).permutation(n)
+        cases.append((f"P{n}", np.eye(n)[p]))
+    for s in range(5):
+        cases.append((f"bern12s{s}", synth.bernoulli(12, s)))
+    for n in (1, 2, 7, 16, 25):
+        cases.append((f"diag1i{n}", synth.diag_1pi(n)))
+    for n in (5, 8):
+        cases.append((f"menage{n}", synth.menage(n)))
+    cases.append(("int9", synth.random_int(9, 7)))
+    return cases
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+@pytest.mark.parametrize("name,A", _e_cases(), ids=[c[0] for c in _e_cases()])
+def test_class_E_bit_exact(name, A, alg):
+    ex = oracle.exact(A, alg)
+    if not ex.fp64_exact_eligible():
+        pytest.skip("exactness precondition not met (class P probe instead)")
+    got = cval((pb.glynn if alg == "glynn" else pb.ryser)(T(A)))
+    assert got == complex(float(ex.value[0]), float(ex.value[1])), (got, ex.value)
+    assert math.copysign(1.0, got.real) > 0 or got.real != 0      # no -0.0
+    assert math.copysign(1.0, got.imag) > 0 or got.imag != 0
+
+
+def test_class_E_diag_1pi_45_range():
+    """P:572 FIG. A3: perm(diag(1+i)_45) = (1+i)^45.  Every Glynn term of a diagonal matrix is
+    (1+i)^n, so a range of k Gray indices sums to k (1+i)^45 = -k 2^22 (1+i) exactly."""
+    A = T(synth.diag_1pi(45))
+    for lo, hi in [(0, 1 << 20), ((1 << 43) + 12345, (1 << 43) + 12345 + 777777)]:
+        d = pb.glynn_range(A, lo, hi).cpu().numpy()
+        k = hi - lo
+        assert d[0] + d[1] == -k * 2.0 ** 22 and d[2] + d[3] == -k * 2.0 ** 22
+
+
+# ----------------------------------------------------------------- class R / B
+def _rel(a: complex, b: complex) -> float:
+    return abs(a - b) / abs(b)
+
+
+@pytest.mark.parametrize("n", list(range(1, 21)) + [22, 24])
+def test_class_R_gaussian_glynn(n):
+    A = synth.gaussian(n, 2000 + n)
+    ref = oracle.glynn(A)
+    got = cval(pb.glynn(T(A)))
+    assert _rel(got, ref.value) <= 1e-9, (_rel(got, ref.value), got, ref.value)
+    c = pb.plan(n).chunk_bits
+    assert abs(got - ref.value) <= (n + 2 ** (c / 2)) * U * ref.l1 + 1e-300
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_class_R_gaussian_n20_seeds(seed):
+    A = synth.gaussian(20, 1000 + seed)
+    ref = oracle.glynn(A)
+    assert _rel(cval(pb.glynn(T(A))), ref.value) <= 1e-9
+
+
+@pytest.mark.parametrize("n", [16, 20, 24])
+def test_class_R_haar_submatrix(n):
+    A = synth.haar_submatrix(n * n, n, 100 + n, 200 + n)
+    ref = oracle.glynn(A)
+    assert _rel(cval(pb.glynn(T(A))), ref.value) <= 1e-9
+
+
+@pytest.mark.slow
+def test_class_R_gaussian_n28():
+    A = synth.gaussian(28, 28)
+    ref = oracle.glynn(A)
+    assert _rel(cval(pb.glynn(T(A))), ref.value) <= 1e-9
+
+
+@pytest.mark.parametrize("n", list(range(1, 19)) + [20, 22])
+def test_ryser_R_or_B(n):
+    A = synth.gaussian(n, 3000 + n)
+    ref = oracle.ryser(A)
+    got = cval(pb.ryser(T(A)))
+    c = pb.plan(n, pb.ALG_RYSER).chunk_bits
+    bound = (n + 2 ** (c / 2)) * U * ref.l1
+    assert _rel(got, ref.value) <= 1e-9 or abs(got - ref.value) <= bound, (_rel(got, ref.value), abs(got - ref.value) / bound)
+
+
+# ----------------------------------------------------------------- ranges, ragged ends, partitions
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+def test_range_partials_ragged(alg):
+    n = 20
+    A = synth.gaussian(n, 77)
+    Tn = 1 << (n - 1 if alg == "glynn" else n)
+    fn = pb.glynn_range if alg == "glynn" else pb.ryser_range
+    ofn = oracle.glynn_partial if alg == "glynn" else oracle.ryser_partial
+    rng = np.random.default_rng(5)
+    cuts = sorted({0, Tn, 1, Tn - 1, 4095, 4096, 4097, *map(int, rng.integers(0, Tn, 6))})
+    dA = T(A)
+    for lo, hi in list(zip(cuts[:-1], cuts[1:])) + [(0, Tn), (3, Tn - 7), (Tn - 1, Tn)]:
+        ref, l1 = ofn(A, lo, hi)
+        got = dd_to_complex(fn(dA, lo, hi))
+        assert abs(got - ref.to_complex()) <= 64 * U * l1 + 1e-300, (lo, hi)
+    assert dd_to_complex(fn(dA, 9, 9)) == 0
+
+
+def test_range_bad_arguments_raise():
+    dA = T(synth.gaussian(10, 1))
+    with pytest.raises(pb.PermError):
+        pb.glynn_range(dA, 5, 4)
+    with pytest.raises(pb.PermError):
+        pb.glynn_range(dA, 0, (1 << 9) + 1)
+    with pytest.raises(pb.PermError):
+        pb.ryser_range(dA, 0, (1 << 10) + 1)
+
+
+@pytest.mark.parametrize("n,alg", [(20, "glynn"), (28, "glynn"), (22, "ryser")])
+def test_canonical_tree_partition_bit_identical(n, alg):
+    """Splitting the unit range into 1/2/4/8 aligned parts (one per GPU), reducing each part to
+    its subtree root and combining the roots reproduces the single-call value bit for bit."""
+    A = T(synth.gaussian(n, 4242))
+    a = pb.ALG_GLYNN if alg == "glynn" else pb.ALG_RYSER
+    full = cval(pb.glynn(A) if alg == "glynn" else pb.ryser(A))
+    P = pb.plan(n, a)
+    for world in (1, 2, 4, 8):
+        if P.units % world:
+            continue
+        roots = []
+        for r in range(world):
+            ulo, uhi = r * P.units // world, (r + 1) * P.units // world
+            parts = pb.sweep_units(A, a, ulo, uhi)
+            roots.append(pb.combine(parts, n, a, scale=False)[1])
+        val, _ = pb.combine(torch.stack(roots), n, a, scale=True)
+        assert cval(val) == full, world
+    # the range API on an aligned half equals the subtree root too
+    half = P.units // 2 * P.unit_terms
+    if P.units >= 2:
+        r0 = (pb.glynn_range if alg == "glynn" else pb.ryser_range)(A, 0, half)
+        sub = pb.combine(pb.sweep_units(A, a, 0, P.units // 2), n, a, scale=False)[1]
+        assert torch.equal(r0, sub)
+
+
+# ----------------------------------------------------------------- invariants (bit-exact)
+@pytest.mark.parametrize("n", [9, 16, 21])
+def test_bit_exact_invariants(n):
+    A = synth.gaussian(n, 31 * n)
+    base = cval(pb.glynn(T(A)))
+    assert cval(pb.glynn(T(-A))) == base * (-1) ** n
+    assert cval(pb.glynn(T(np.conj(A)))) == base.conjugate()
+    B = A.copy()
+    B[n // 2] *= 2.0
+    assert cval(pb.glynn(T(B))) == 2 * base
+    assert cval(pb.glynn(T(A * 0.5))) == base * 0.5 ** n
+    rb = cval(pb.ryser(T(A)))
+    assert cval(pb.ryser(T(np.conj(A)))) == rb.conjugate()
+
+
+def test_invariants_to_rounding():
+    n = 18
+    A = synth.gaussian(n, 5)
+    base = cval(pb.glynn(T(A)))
+    p = np.random.default_rng(1).permutation(n)
+    for B, f in ((A.T, 1), (A[p], 1), (A[:, p], 1), (1j * A, 1j ** n)):
+        assert _rel(cval(pb.glynn(T(B))), base * f) <= 1e-11
+
+
+# ----------------------------------------------------------------- batched
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 6, 7, 10, 13, 16, 18])
+def test_batched_small(n):
+    As = np.stack([synth.gaussian(n, 50 * n + b) for b in range(24)])
+    got = pb.glynn_batched(T(As)).cpu().numpy()
+    for b in range(As.shape[0]):
+        ref = oracle.glynn(As[b])
+        assert _rel(complex(got[b]), ref.value) <= 1e-9, (n, b)
+
+
+def test_batched_integer_bit_exact_and_empty():
+    As = np.stack([synth.bernoulli(12, s) for s in range(5)] + [synth.ones(12), synth.ones_minus_eye(12)])
+    got = pb.glynn_batched(T(As)).cpu().numpy()
+    for b in range(As.shape[0]):
+        ex = oracle.exact(As[b]).value
+        assert complex(got[b]) == complex(float(ex[0]), float(ex[1]))
+    empty = pb.glynn_batched(torch.zeros((0, 16, 16), dtype=torch.complex128, device=DEV))
+    assert empty.shape == (0,)
+
+
+def test_batched_haar_sample_vs_oracle():
+    As = synth.haar_batch(256, 256, 16, 16, 17)
+    got = pb.glynn_batched(T(As)).cpu().numpy()
+    for b in range(0, 256, 5):
+        ref = oracle.glynn(As[b])
+        assert _rel(complex(got[b]), ref.value) <= 1e-9
+
+
+# ----------------------------------------------------------------- host-buffer entry points
+def test_host_entry_points():
+    A = synth.gaussian(14, 3)
+    ref = oracle.glynn(A).value
+    assert _rel(pb.glynn_host(A), ref) <= 1e-9
+    assert _rel(pb.ryser_host(A), ref) <= 1e-9
+    As = np.stack([synth.gaussian(10, s) for s in range(4)])
+    got = pb.glynn_batched_host(As)
+    for b in range(4):
+        assert _rel(complex(got[b]), oracle.glynn(As[b]).value) <= 1e-9
+
+
+# ----------------------------------------------------------------- maximum sizes (n up to 64)
+@pytest.mark.parametrize("n", [45, 50, 56, 60, 64])
+def test_large_n_ranges_vs_oracle(n):
+    """Large-n kernels (the M5 n=50 instantiation and the register-spilling n > 56 ones) on
+    windows the oracle can walk: aligned, ragged, and crossing chunk boundaries."""
+    A = synth.gaussian(n, 9000 + n)
+    dA = T(A)
+    P = pb.plan(n)
+    chunk = 1 << P.chunk_bits
+    for lo, hi in [(0, 4 * chunk), (P.terms - 3 * chunk - 5, P.terms), (7 * chunk + 3, 9 * chunk + 1)]:
+        ref, l1 = oracle.glynn_partial(A, lo, hi)
+        got = dd_to_complex(pb.glynn_range(dA, lo, hi))
+        assert abs(got - ref.to_complex()) <= (n + 2 ** (P.chunk_bits / 2)) * U * l1, (lo, hi)
+    Pr = pb.plan(n, pb.ALG_RYSER)
+    lo, hi = Pr.terms - 2 * chunk, Pr.terms
+    ref, l1 = oracle.ryser_partial(A, lo, hi)
+    got = dd_to_complex(pb.ryser_range(dA, lo, hi))
+    assert abs(got - ref.to_complex()) <= (n + 2 ** (Pr.chunk_bits / 2)) * U * l1
