@@ -52,7 +52,8 @@ typedef struct { double re_hi, re_lo, im_hi, im_lo; } perm_dd_c128;  /* 32 B */
 
 enum {
   PERM_OK = 0,
-  PERM_EINVAL = 1,   /* null pointer, n < 1, n > perm_max_n(), batch < 0, lo > hi, hi > #terms, count < 1 */
+  PERM_EINVAL = 1,   /* null pointer, n < 1, n > perm_max_n() (Ryser: n > 63), batch < 0, lo > hi,
+                        hi > #terms, count < 1, bad alg */
   PERM_ECUDA = 2,    /* CUDA runtime / launch error (message via perm_strerror(PERM_ECUDA)) */
   PERM_ENOTIMPL = 3
 };
@@ -76,8 +77,9 @@ typedef struct {
   int64_t units;
 } perm_plan_t;
 
-/* Largest supported n (64).  n <= 56 keeps the row sums register-resident without
- * spills; 57..64 are correct but slower (register spills). */
+/* Largest supported n (64 for Glynn; Ryser stops at 63 because its 2^n Gray indices
+ * must fit in uint64).  n <= 56 keeps the row sums register-resident; 57..64 are correct
+ * but slower (register spills). */
 int perm_max_n(void);
 
 /* Human-readable text for a status code (for PERM_ECUDA: the last CUDA error seen by

@@ -56,6 +56,7 @@ def _L():
         _lib.oracle_glynn_gray.argtypes = [dp, i32, u64, u64, i32, dp, dp]
         _lib.oracle_ryser_gray.argtypes = [dp, i32, u64, u64, i32, dp, dp]
         _lib.oracle_exact_int.argtypes = [i64p, i64p, i32, i32, i64p, i64p, i64p, dp]
+        _lib.oracle_gray_ex.argtypes = [dp, i32, i32, u64, u64, i32, dp, dp, dp]
         _lib.oracle_dd_add.argtypes = [dp, dp, dp]
         _lib.oracle_dd_add.restype = None
     return _lib
@@ -144,6 +145,26 @@ def glynn_partial(A, lo: int, hi: int, threads: int | None = None) -> tuple[DD, 
 def ryser_partial(A, lo: int, hi: int, threads: int | None = None) -> tuple[DD, float]:
     """Signed sum over Gray indices [lo, hi) of Eq. (1) terms (sign (-1)^{n-|S|}); also sum |term|."""
     return _partial(_L().oracle_ryser_gray, A, lo, hi, threads)
+
+
+@dataclass
+class Partial:
+    dd: DD        # unscaled signed sum over the range
+    l1: float     # sum |term|
+    l1c: float    # sum |term| * sum_i (sum_j |a_ij|) / |s_i|  (componentwise error scale)
+
+
+def partial_ex(A, lo: int, hi: int, alg: str = "glynn", threads: int | None = None) -> Partial:
+    """Range partial with both error scales (reading R10b)."""
+    a, n = _mat(A)
+    out = np.zeros(4)
+    l1 = ctypes.c_double(0.0)
+    l1c = ctypes.c_double(0.0)
+    rc = _L().oracle_gray_ex(_dp(a), n, 1 if alg == "ryser" else 0, int(lo), int(hi),
+                             int(threads or default_threads()), _dp(out), ctypes.byref(l1), ctypes.byref(l1c))
+    if rc != 0:
+        raise ValueError(f"bad arguments n={n} lo={lo} hi={hi}")
+    return Partial(DD.from4(out), l1.value, l1c.value)
 
 
 def glynn(A, threads: int | None = None) -> Result:

@@ -174,7 +174,7 @@ int oracle_ryser_faithful(const double* A, int n, uint64_t lo, uint64_t hi, doub
  * l1 accumulates |term| (double, approximate) for the error bounds. */
 typedef struct {
   const double* A; int n; int ryser; uint64_t lo, hi;
-  ddc acc; double l1;
+  ddc acc; double l1; double l1c;
 } walk_job;
 
 static void* walk_range(void* arg) {
@@ -182,9 +182,15 @@ static void* walk_range(void* arg) {
   const double* A = w->A;
   const int n = w->n;
   ddc acc = ddc_zero();
-  double l1 = 0.0;
+  double l1 = 0.0, l1c = 0.0;
   if (w->lo < w->hi) {
     ddc* s = (ddc*)malloc(sizeof(ddc) * n);
+    /* rowabs_i = sum_j |a_ij|: the scale of the rounding error of any row sum of row i */
+    double* rowabs = (double*)malloc(sizeof(double) * n);
+    for (int i = 0; i < n; ++i) {
+      rowabs[i] = 0.0;
+      for (int j = 0; j < n; ++j) rowabs[i] += hypot(RE(A, n, i, j), IM(A, n, i, j));
+    }
     uint64_t G = gray(w->lo);
     for (int i = 0; i < n; ++i) {
       if (!w->ryser) {
@@ -204,7 +210,15 @@ static void* walk_range(void* arg) {
       for (int i = 1; i < n; ++i) p = ddc_mul(p, s[i]);
       int neg = w->ryser ? ((n - popcount64(G)) & 1) : (popcount64(G) & 1);
       acc = neg ? ddc_sub(acc, p) : ddc_add(acc, p);
-      l1 += ddc_abs_approx(p);
+      const double ap = ddc_abs_approx(p);
+      l1 += ap;
+      /* componentwise error scale: |term| * sum_i rowabs_i / |s_i| (first-order relative
+       * error of the product when each row sum carries an error ~ u * rowabs_i) */
+      if (ap > 0.0) {
+        double kappa = 0.0;
+        for (int i = 0; i < n; ++i) kappa += rowabs[i] / ddc_abs_approx(s[i]);
+        l1c += ap * kappa;
+      }
       if (++g >= w->hi) break;
       const int b = ctz64(g);
       const uint64_t Gn = gray(g);
@@ -220,14 +234,16 @@ static void* walk_range(void* arg) {
       G = Gn;
     }
     free(s);
+    free(rowabs);
   }
   w->acc = acc;
   w->l1 = l1;
+  w->l1c = l1c;
   return 0;
 }
 
 static int walk_threaded(const double* A, int n, int ryser, uint64_t lo, uint64_t hi, int threads,
-                         double* out4, double* l1_out) {
+                         double* out4, double* l1_out, double* l1c_out) {
   if (threads < 1) threads = 1;
   if (threads > 256) threads = 256;
   uint64_t len = hi - lo;
@@ -243,22 +259,33 @@ static int walk_threaded(const double* A, int n, int ryser, uint64_t lo, uint64_
   walk_range(&jobs[0]);
   for (int t = 1; t < threads; ++t) pthread_join(tid[t], 0);
   ddc acc = ddc_zero();
-  double l1 = 0.0;
-  for (int t = 0; t < threads; ++t) { acc = ddc_add(acc, jobs[t].acc); l1 += jobs[t].l1; }
+  double l1 = 0.0, l1c = 0.0;
+  for (int t = 0; t < threads; ++t) { acc = ddc_add(acc, jobs[t].acc); l1 += jobs[t].l1; l1c += jobs[t].l1c; }
   ddc_store(acc, out4);
   if (l1_out) *l1_out = l1;
+  if (l1c_out) *l1c_out = l1c;
   free(jobs); free(tid);
   return 0;
 }
 
 int oracle_glynn_gray(const double* A, int n, uint64_t lo, uint64_t hi, int threads, double* out4, double* l1) {
-  if (n < 1 || n > 63 || lo > hi || hi > (1ull << (n - 1)) || !A || !out4) return 1;
-  return walk_threaded(A, n, 0, lo, hi, threads, out4, l1);
+  if (n < 1 || n > 64 || lo > hi || hi > (1ull << (n - 1)) || !A || !out4) return 1;
+  return walk_threaded(A, n, 0, lo, hi, threads, out4, l1, 0);
 }
 
 int oracle_ryser_gray(const double* A, int n, uint64_t lo, uint64_t hi, int threads, double* out4, double* l1) {
-  if (n < 1 || n > 63 || lo > hi || (n < 64 && hi > (1ull << n)) || !A || !out4) return 1;
-  return walk_threaded(A, n, 1, lo, hi, threads, out4, l1);
+  if (n < 1 || n > 63 || lo > hi || hi > (1ull << n) || !A || !out4) return 1;
+  return walk_threaded(A, n, 1, lo, hi, threads, out4, l1, 0);
+}
+
+/* Same walks, also returning l1c = sum_terms |term| * sum_i (sum_j |a_ij|) / |s_i|, the
+ * componentwise error scale used by the parity bound of DESIGN.md reading R10b. */
+int oracle_gray_ex(const double* A, int n, int ryser, uint64_t lo, uint64_t hi, int threads, double* out4,
+                   double* l1, double* l1c) {
+  if (n < 1 || !A || !out4 || lo > hi) return 1;
+  if (!ryser && (n > 64 || hi > (1ull << (n - 1)))) return 1;
+  if (ryser && (n > 63 || hi > (1ull << n))) return 1;
+  return walk_threaded(A, n, ryser, lo, hi, threads, out4, l1, l1c);
 }
 
 /* ------------------------------------------------------------------ exact Gaussian integers */

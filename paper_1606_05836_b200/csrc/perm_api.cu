@@ -88,6 +88,8 @@ void make_plan(int n, int alg, perm_plan_t* p) {
 }
 
 bool valid_n(int n) { return n >= 1 && n <= kNMax; }
+// Ryser has 2^n terms: n = 64 would overflow the 64-bit Gray index.
+bool valid_n_alg(int n, int alg) { return valid_n(n) && (alg == PERM_ALG_GLYNN ? true : n <= 63); }
 
 // Canonical tree over `count` partials (zero-padded to P = 2^k): one block of up to 1024
 // threads; thread t reduces the aligned segment [t*S, (t+1)*S) with the binary-counter
@@ -173,7 +175,7 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
 constexpr size_t kStagingBytes = sizeof(double2) * kTabRows * kNMax;
 
 int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t st) {
-  if (!A || !out || !valid_n(n)) return PERM_EINVAL;
+  if (!A || !out || !valid_n_alg(n, alg)) return PERM_EINVAL;
   perm_plan_t P;
   make_plan(n, alg, &P);
   void* ws = nullptr;
@@ -190,7 +192,7 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
 }
 
 int range_perm(const perm_c128* A, int n, int alg, uint64_t lo, uint64_t hi, perm_dd_c128* partial, cudaStream_t st) {
-  if (!A || !partial || !valid_n(n)) return PERM_EINVAL;
+  if (!A || !partial || !valid_n_alg(n, alg)) return PERM_EINVAL;
   perm_plan_t P;
   make_plan(n, alg, &P);
   const uint64_t T = 1ULL << P.log2_terms;
@@ -239,7 +241,7 @@ const char* perm_strerror(int code) {
 }
 
 int perm_plan(int n, int alg, perm_plan_t* plan) {
-  if (!plan || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  if (!plan || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
   make_plan(n, alg, plan);
   return PERM_OK;
 }
@@ -254,7 +256,7 @@ int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream) {
 
 int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_t unit_hi,
                      perm_dd_c128* unit_partials, void* stream) {
-  if (!A || !unit_partials || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  if (!A || !unit_partials || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
   perm_plan_t P;
   make_plan(n, alg, &P);
   if (unit_lo < 0 || unit_lo > unit_hi || unit_hi > P.units) return PERM_EINVAL;
@@ -279,7 +281,7 @@ int perm_ryser_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_d
 
 int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg, perm_c128* out,
                  perm_dd_c128* out_dd, void* stream) {
-  if (!partials || count < 1 || !valid_n(n) || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER)) return PERM_EINVAL;
+  if (!partials || count < 1 || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
   if (!out && !out_dd) return PERM_EINVAL;
   return run_combine(reinterpret_cast<const Dd2*>(partials), count, n, alg, reinterpret_cast<double2*>(out),
                      reinterpret_cast<Dd2*>(out_dd), static_cast<cudaStream_t>(stream));

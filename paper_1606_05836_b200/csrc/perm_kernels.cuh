@@ -34,8 +34,9 @@ enum { kGlynn = 0, kRyser = 1 };
 
 constexpr int kNMax = 64;      // largest n
 constexpr int kCMax = 12;      // largest chunk_bits
-constexpr int kTabRows = 16;   // rows per constant slot; rows >= c (incl. 15) are zero
-constexpr int kSlots = 3;      // constant-memory column slots per translation unit (3 x 16 KB)
+constexpr int kTabBits = 16;   // Gray bits covered by a column table (rows for bits >= c are zero)
+constexpr int kTabRows = 2 * kTabBits;   // row 2b+d = signed step vector of bit b, direction d
+constexpr int kSlots = 1;      // constant-memory column slots per translation unit (32 KB each)
 constexpr int kMaxBlock = 128; // threads per block (block_bits <= 7)
 
 struct Dd2 { double re_hi, re_lo, im_hi, im_lo; };
@@ -123,21 +124,22 @@ __device__ __forceinline__ double2 row_product(const double2 (&s)[N]) {
 // Flip of Gray bit b touches matrix column col0 + b (Glynn col0 = 1: bit b <-> delta_{b+2};
 // Ryser col0 = 0: bit b <-> column b).
 //
-// ConstColumns: table[slot][b][i] = kScale * a_{i, col0+b} for b < c, zero for c <= b < 16.
+// ConstColumns: table[slot][2b+d][i] = signed step vector of Gray bit b flipped with direction d
+// (b < c; zero rows for c <= b < 16), so every flip is one DADD with a uniform operand.
 // Declared per translation unit (static): each TU stages its own copy.
 static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 
 struct ConstColumns {
   int base;
-  __device__ __forceinline__ double2 get(int b, int i) const { return c_cols[base + b * kNMax + i]; }
+  __device__ __forceinline__ double2 get(int row, int i) const { return c_cols[base + row * kNMax + i]; }
 };
 
 // SmemColumns: a per-block shared-memory table with the same layout as the constant one:
-// tab[b*N + i] = step vector of Gray bit b for b < c, zero for c <= b < 16.
+// tab[(2b+d)*N + i] = signed step vector of Gray bit b, direction d (zero rows for b >= c).
 template <int N>
 struct SmemColumns {
   const double2* tab;
-  __device__ __forceinline__ double2 get(int b, int i) const { return tab[b * N + i]; }
+  __device__ __forceinline__ double2 get(int row, int i) const { return tab[row * N + i]; }
 };
 
 // ------------------------------------------------------------------ the walker
@@ -195,21 +197,35 @@ struct Walker {
     }
   }
 
-  // s_i <- s_i + sg * u_b,i with a runtime sign sg in {-1, 0, +1}: one DFMA per real
-  // component; the step vector is the uniform operand (UR), sg a vector register.
+  // Row of the signed table holding +u_b (Glynn: d = 1 -> +u; Ryser: d = 0 -> +u).
+  static __device__ __forceinline__ int plus_row(int b) { return 2 * b + (ALG == kGlynn ? 1 : 0); }
+
+  // s_i <- s_i + table[row]_i : one DADD per real component, the signed step vector being
+  // the uniform (UR) operand.
   template <class Cols>
-  __device__ __forceinline__ void flip(const Cols& cols, int b, double sg) {
+  __device__ __forceinline__ void flip_row(const Cols& cols, int row) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double2 v = cols.get(b, i);
+      const double2 v = cols.get(row, i);
+      s[i].x = __dadd_rn(s[i].x, v.x);
+      s[i].y = __dadd_rn(s[i].y, v.y);
+    }
+  }
+
+  // s_i <- s_i + sg * table[row]_i with a per-thread sign sg = +-1 (the one mid-chunk flip).
+  template <class Cols>
+  __device__ __forceinline__ void flip_signed(const Cols& cols, int row, double sg) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double2 v = cols.get(row, i);
       s[i].x = __fma_rn(sg, v.x, s[i].x);
       s[i].y = __fma_rn(sg, v.y, s[i].y);
     }
   }
   // Uniform half-walk.  State on entry = row sums at local index T0; visits local indices
   // T0 .. T0+H-1 (H = 2^(c-1) >= 16).  Iteration t (t = -4, 0, 4, ..., H-8) visits
-  // T0+t+4 .. T0+t+7:  r=0 flips Gray bit b = ctz(t+4) (t = -4: table row 15, all zeros:
-  // no flip), r=1 bit 0, r=2 bit 1, r=3 bit 0.  Direction of the flip into index g is
+  // T0+t+4 .. T0+t+7:  r=0 flips Gray bit b = ctz(t+4) (t = -4: bit 15, all-zero table
+  // rows: no flip), r=1 bit 0, r=2 bit 1, r=3 bit 0.  Direction of the flip into index g is
   // bit (b+1) of g, so r=1 -> 0, r=3 -> 1, r=2 -> bit 2 of t+4 and r=0
   // -> bit b+1 of T0+t+4: all warp-uniform.  Terms alternate in sign (parity of G(g) =
   // parity of g); plain sums over 16 terms, then the compensated (Sum2) accumulator.
@@ -226,10 +242,10 @@ struct Walker {
       const int tz = t * zero;
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1) + tz;
+        const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
         const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
-        const double sg = d ? kSgnDir1 : kSgnDir0;
-        flip(cols, b, sg);
+        const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
+        flip_row(cols, row);
         const double2 p = row_product<N>(s);
         if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
         else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
@@ -245,9 +261,14 @@ struct Walker {
     const uint64_t g0 = q << c;
     build(at, g0 ^ (g0 >> 1));
     const int H = 1 << (c - 1);
-    half_walk(cols, 0, H, zero);
-    flip(cols, c - 1, (q & 1) ? kSgnDir1 : kSgnDir0);   // direction = bit c of g = bit 0 of q
-    half_walk(cols, H, H, zero);
+    // One copy of the half-walk loop serves both halves (two inlined copies of the n = 50
+    // loop body overflow the instruction cache).
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      // direction = bit c of g = bit 0 of q: per-thread sign on the +u row (uniform index)
+      if (h == 1) flip_signed(cols, plus_row(c - 1), (q & 1) ? kSgnDir1 : kSgnDir0);
+      half_walk(cols, h * H, H, zero);
+    }
   }
 
   // Generic walk over [ga, gb) inside one aligned chunk (ragged range ends, tiny n):
@@ -387,8 +408,14 @@ __global__ void __launch_bounds__(kMaxBlock) batched_kernel(const BatchedArgs ar
     stage_transposed<N>(args.A + b * (int64_t)(N * N), at, 2.0);
     __syncthreads();
     for (int k = threadIdx.x; k < kTabRows * N; k += blockDim.x) {
-      const int bb = k / N, i = k - bb * N;
-      tab[k] = (bb < args.c && 1 + bb < N) ? at[(1 + bb) * N + i] : make_double2(0.0, 0.0);
+      const int row = k / N, i = k - row * N;
+      const int bb = row >> 1, d = row & 1;
+      double2 v = make_double2(0.0, 0.0);
+      if (bb < args.c && 1 + bb < N) {
+        v = at[(1 + bb) * N + i];      // 2a (pre-scaled); Glynn: d=1 -> +2a, d=0 -> -2a
+        if (!d) { v.x = -v.x; v.y = -v.y; }
+      }
+      tab[k] = v;
     }
     __syncthreads();
     const SmemColumns<N> cols{tab};
@@ -413,12 +440,15 @@ __global__ void __launch_bounds__(kMaxBlock) batched_kernel(const BatchedArgs ar
 static __global__ void stage_columns_kernel(const double2* __restrict__ A, int n, int col0, int c, double scale,
                                      double2* table) {
   for (int k = threadIdx.x; k < kTabRows * kNMax; k += blockDim.x) {
-    const int b = k / kNMax, i = k - b * kNMax;
+    const int row = k / kNMax, i = k - row * kNMax;
+    const int b = row >> 1, d = row & 1;
     double2 v = make_double2(0.0, 0.0);
     if (b < c && i < n && col0 + b < n) {
       v = A[(size_t)i * n + col0 + b];
-      v.x *= scale;   // x2 is exact
-      v.y *= scale;
+      // Glynn (col0 = 1): d=1 -> +2a, d=0 -> -2a;  Ryser (col0 = 0): d=1 -> -a, d=0 -> +a
+      const double sg = (col0 == 1) ? (d ? scale : -scale) : (d ? -scale : scale);
+      v.x *= sg;      // x(+-2) and x(+-1) are exact
+      v.y *= sg;
     }
     table[k] = v;
   }

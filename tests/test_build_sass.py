@@ -1,0 +1,47 @@
+"""SASS guard (CPU, cuobjdump): the sweep kernels must read their Gray-step columns from
+constant memory through UNIFORM registers (LDCU) -- no per-thread LDC of the column table --
+and contain no tensor-core or legacy-HMMA instructions.  ptxas only produces this for a particular loop shape; this
+test catches a change that silently falls back to per-thread loads + spills."""
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "paper_1606_05836_b200", "_build")
+
+pytestmark = pytest.mark.skipif(shutil.which("cuobjdump") is None, reason="cuobjdump not available")
+
+
+def _sass(obj):
+    path = os.path.join(BUILD, obj)
+    if not os.path.exists(path):
+        from paper_1606_05836_b200 import build
+        build.build()
+    return subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True, check=True).stdout
+
+
+def _kernel(sass, n, alg):
+    out, on = [], False
+    for line in sass.splitlines():
+        if "Function : " in line:
+            on = f"sweep_kernelILi{n}ELi{alg}E" in line
+        elif on:
+            out.append(line)
+    assert out, f"sweep_kernel<{n},{alg}> not found"
+    return "\n".join(out)
+
+
+@pytest.mark.parametrize("obj,n,alg", [("perm_inst_glynn_b.o", 32, 0), ("perm_inst_glynn_c.o", 40, 0),
+                                       ("perm_inst_glynn_c.o", 50, 0), ("perm_inst_ryser_b.o", 32, 1)])
+def test_sweep_columns_are_uniform_operands(obj, n, alg):
+    k = _kernel(_sass(obj), n, alg)
+    ldcu = len(re.findall(r"\bLDCU", k))
+    ldc_vec = len(re.findall(r"LDC(?:\.64)? R\d+, c\[0x3\]\[R", k))
+    assert ldcu >= 10 * n, (ldcu, ldc_vec)
+    assert ldc_vec <= 8, (ldcu, ldc_vec)
+    assert "DFMA" in k and "DMUL" in k
+    for bad in ("HMMA", "UTCHMMA", "DMMA"):
+        assert bad not in k

@@ -1,0 +1,126 @@
+"""BASELINE.json configs at full size, in the launch configuration bench.py times, checked
+against values the oracle computes (stored under tests/golden/ by tools/make_golden.py, which
+calls only oracle/) or, where the oracle cannot walk the whole sum, on sampled units /
+windows the oracle computes one by one, and on closed-form properties that hold at any size.
+
+  M1  n=20 Gaussian, Glynn + Ryser, plus 0/1 checks            (test_gpu_parity covers J/J-I/Bernoulli)
+  M2  4096 x 16x16 Haar(256) submatrices, batched               all 4096 vs golden
+  M3  n=32 Gaussian, Glynn + Ryser                              full value vs golden (oracle ~1 core-hour)
+  M4  n=40 Haar(1600) submatrix, the bench workload             sampled canonical units vs oracle;
+                                                                block-diagonal 20+20 pin at n=40
+  M5  n=50 Gaussian                                             sampled windows vs oracle
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+import paper_1606_05836_b200 as pb
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+U = 2.0 ** -53
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).to(DEV)
+
+
+def _dd(hexes):
+    v = [float.fromhex(h) for h in hexes]
+    return complex(v[0] + v[1], v[2] + v[3])
+
+
+def _bound(part, n, c, scale=1.0):
+    return U * ((math.sqrt(n) + 2 ** (c / 2)) * part.l1c + (3 * n + 16) * part.l1) * scale
+
+
+def test_m1_glynn_ryser():
+    A = synth.workload("M1")
+    ref = oracle.glynn(A).value
+    g = complex(pb.glynn(T(A)).item())
+    assert abs(g - ref) <= 1e-9 * abs(ref)
+    part = oracle.partial_ex(A, 0, 1 << 20, "ryser")
+    r = complex(pb.ryser(T(A)).item())
+    assert abs(r - ref) <= 1e-9 * abs(ref) or abs(r - part.dd.to_complex()) <= _bound(part, 20, pb.plan(20, 1).chunk_bits)
+
+
+def test_m2_batched_all_4096_vs_golden():
+    with open(os.path.join(GOLDEN, "m2_batched_n16.json")) as f:
+        gold = json.load(f)
+    As = synth.workload("M2")
+    assert synth.sha256(As) == gold["sha256"], "input bytes differ from the golden file's"
+    got = pb.glynn_batched(T(As)).cpu().numpy()
+    worst = 0.0
+    for b, v in enumerate(gold["values"]):
+        ref = _dd(v["dd"])
+        rel = abs(got[b] - ref) / abs(ref)
+        worst = max(worst, rel)
+        assert rel <= 1e-9, (b, rel)
+    assert worst < 1e-11
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+def test_m3_n32_vs_golden(alg):
+    path = os.path.join(GOLDEN, "m3_n32.json")
+    if not os.path.exists(path):
+        pytest.skip("golden value not generated")
+    with open(path) as f:
+        gold = json.load(f)
+    if alg not in gold:
+        pytest.skip("golden value not generated")
+    A = synth.workload("M3")
+    assert synth.sha256(A) == gold["sha256"]
+    ref = _dd(gold[alg]["dd"])
+    got = complex((pb.glynn if alg == "glynn" else pb.ryser)(T(A)).item())
+    rel = abs(got - ref) / abs(ref)
+    if alg == "glynn":
+        assert rel <= 1e-9, rel
+    else:   # report-only precision probe beyond 1e-9 is the paper's finding; bound by L1 (class B)
+        c = pb.plan(32, pb.ALG_RYSER).chunk_bits
+        assert rel <= 1e-9 or abs(got - ref) <= (math.sqrt(32) + 2 ** (c / 2)) * 64 * U * gold[alg]["l1"], rel
+
+
+def test_m4_sampled_units_vs_oracle():
+    """bench.py's workload and launch: canonical units of plan(40) computed by the same sweep
+    kernel, compared one by one with the oracle's walk over the same Gray-index ranges."""
+    A = synth.workload("M4")
+    dA = T(A)
+    P = pb.plan(40)
+    for u in (0, 1, 77777, P.units - 1):
+        got = pb.sweep_units(dA, pb.ALG_GLYNN, u, u + 1).cpu().numpy()[0]
+        part = oracle.partial_ex(A, u * P.unit_terms, (u + 1) * P.unit_terms)
+        g = complex(got[0] + got[1], got[2] + got[3])
+        assert abs(g - part.dd.to_complex()) <= _bound(part, 40, P.chunk_bits), u
+
+
+@pytest.mark.slow
+def test_m4_block_diagonal_pin_n40():
+    """Full n=40 sweep (the bench kernel, 2^39 terms): perm(A1 (+) A2) = perm(A1) perm(A2)
+    with the 20x20 factors from the oracle."""
+    A1 = synth.haar_submatrix(400, 20, 1, 2)
+    A2 = synth.haar_submatrix(400, 20, 3, 4)
+    want = oracle.glynn(A1).value * oracle.glynn(A2).value
+    got = complex(pb.glynn(T(synth.block_diag(A1, A2))).item())
+    assert abs(got - want) <= 1e-9 * abs(want)
+
+
+def test_m5_windows_vs_oracle():
+    A = synth.workload("M5")
+    dA = T(A)
+    for alg in ("glynn", "ryser"):
+        a = pb.ALG_GLYNN if alg == "glynn" else pb.ALG_RYSER
+        P = pb.plan(50, a)
+        fn = pb.glynn_range if alg == "glynn" else pb.ryser_range
+        for lo in (0, P.unit_terms * 12345 + 999, P.terms - (1 << 16)):
+            hi = lo + (1 << 16)
+            part = oracle.partial_ex(A, lo, hi, alg)
+            d = fn(dA, lo, hi).cpu().numpy()
+            g = complex(d[0] + d[1], d[2] + d[3])
+            assert abs(g - part.dd.to_complex()) <= _bound(part, 50, P.chunk_bits), (alg, lo)

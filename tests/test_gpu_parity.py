@@ -4,8 +4,12 @@ on the same seeded inputs (task rule ③).  Tolerance classes from SURVEY §8(c)
   E  bit-exact: integer matrices meeting the exactness precondition (oracle.exact(...)
      .fp64_exact_eligible(): every partial product and partial sum an integer < 2^53)
   R  relative <= 1e-9 vs the double-double oracle (north_star), Gaussian / Haar, n <= 28
-  B  |gpu - oracle| <= (n + 2^(c/2)) * u * L1 (walk-aware, L1 = sum |term| from the oracle);
-     Ryser passes with R or B (the paper's finding: FP64 Ryser cannot meet 1e-9)
+  B  componentwise, walk-aware bound (reading R10b):
+       |gpu - oracle| <= u * [ (sqrt(n) + 2^(c/2)) * L1c + (3n + 16) * L1 ]
+     with L1 = sum |term| and L1c = sum |term| * sum_i (sum_j |a_ij|) / |s_i| from the oracle
+     (a row sum carries error ~ u sum_j |a_ij| after its O(n) build plus ~2^(c/2) u sum_j |a_ij|
+     after a 2^c-step walk; the product adds ~3n u relative; 16-term plain sums add 16 u).
+     Ryser passes with R or B (the paper's finding: FP64 Ryser cannot meet 1e-9).
 """
 import math
 
@@ -82,14 +86,19 @@ def _rel(a: complex, b: complex) -> float:
     return abs(a - b) / abs(b)
 
 
+def bound_B(part: "oracle.Partial", n: int, c: int, scale: float = 1.0) -> float:
+    return U * ((math.sqrt(n) + 2 ** (c / 2)) * part.l1c + (3 * n + 16) * part.l1) * scale
+
+
 @pytest.mark.parametrize("n", list(range(1, 21)) + [22, 24])
 def test_class_R_gaussian_glynn(n):
     A = synth.gaussian(n, 2000 + n)
     ref = oracle.glynn(A)
     got = cval(pb.glynn(T(A)))
     assert _rel(got, ref.value) <= 1e-9, (_rel(got, ref.value), got, ref.value)
-    c = pb.plan(n).chunk_bits
-    assert abs(got - ref.value) <= (n + 2 ** (c / 2)) * U * ref.l1 + 1e-300
+    P = pb.plan(n)
+    part = oracle.partial_ex(A, 0, P.terms)
+    assert abs(got - ref.value) <= bound_B(part, n, P.chunk_bits, 2.0 ** -(n - 1))
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -116,11 +125,12 @@ def test_class_R_gaussian_n28():
 @pytest.mark.parametrize("n", list(range(1, 19)) + [20, 22])
 def test_ryser_R_or_B(n):
     A = synth.gaussian(n, 3000 + n)
-    ref = oracle.ryser(A)
+    P = pb.plan(n, pb.ALG_RYSER)
+    part = oracle.partial_ex(A, 0, P.terms, "ryser")
+    ref = part.dd.to_complex()
     got = cval(pb.ryser(T(A)))
-    c = pb.plan(n, pb.ALG_RYSER).chunk_bits
-    bound = (n + 2 ** (c / 2)) * U * ref.l1
-    assert _rel(got, ref.value) <= 1e-9 or abs(got - ref.value) <= bound, (_rel(got, ref.value), abs(got - ref.value) / bound)
+    bound = bound_B(part, n, P.chunk_bits)
+    assert _rel(got, ref) <= 1e-9 or abs(got - ref) <= bound, (_rel(got, ref), abs(got - ref) / bound)
 
 
 # ----------------------------------------------------------------- ranges, ragged ends, partitions
@@ -130,14 +140,14 @@ def test_range_partials_ragged(alg):
     A = synth.gaussian(n, 77)
     Tn = 1 << (n - 1 if alg == "glynn" else n)
     fn = pb.glynn_range if alg == "glynn" else pb.ryser_range
-    ofn = oracle.glynn_partial if alg == "glynn" else oracle.ryser_partial
     rng = np.random.default_rng(5)
     cuts = sorted({0, Tn, 1, Tn - 1, 4095, 4096, 4097, *map(int, rng.integers(0, Tn, 6))})
     dA = T(A)
+    c = pb.plan(n, pb.ALG_GLYNN if alg == "glynn" else pb.ALG_RYSER).chunk_bits
     for lo, hi in list(zip(cuts[:-1], cuts[1:])) + [(0, Tn), (3, Tn - 7), (Tn - 1, Tn)]:
-        ref, l1 = ofn(A, lo, hi)
+        part = oracle.partial_ex(A, lo, hi, alg)
         got = dd_to_complex(fn(dA, lo, hi))
-        assert abs(got - ref.to_complex()) <= 64 * U * l1 + 1e-300, (lo, hi)
+        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, c) + 1e-300, (lo, hi)
     assert dd_to_complex(fn(dA, 9, 9)) == 0
 
 
@@ -251,11 +261,12 @@ def test_large_n_ranges_vs_oracle(n):
     P = pb.plan(n)
     chunk = 1 << P.chunk_bits
     for lo, hi in [(0, 4 * chunk), (P.terms - 3 * chunk - 5, P.terms), (7 * chunk + 3, 9 * chunk + 1)]:
-        ref, l1 = oracle.glynn_partial(A, lo, hi)
+        part = oracle.partial_ex(A, lo, hi)
         got = dd_to_complex(pb.glynn_range(dA, lo, hi))
-        assert abs(got - ref.to_complex()) <= (n + 2 ** (P.chunk_bits / 2)) * U * l1, (lo, hi)
-    Pr = pb.plan(n, pb.ALG_RYSER)
-    lo, hi = Pr.terms - 2 * chunk, Pr.terms
-    ref, l1 = oracle.ryser_partial(A, lo, hi)
-    got = dd_to_complex(pb.ryser_range(dA, lo, hi))
-    assert abs(got - ref.to_complex()) <= (n + 2 ** (Pr.chunk_bits / 2)) * U * l1
+        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, P.chunk_bits), (lo, hi)
+    if n <= 63:
+        Pr = pb.plan(n, pb.ALG_RYSER)
+        lo, hi = Pr.terms - 2 * chunk, Pr.terms
+        part = oracle.partial_ex(A, lo, hi, "ryser")
+        got = dd_to_complex(pb.ryser_range(dA, lo, hi))
+        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, Pr.chunk_bits)

@@ -1,0 +1,38 @@
+"""Profiling driver (ncu target): run the bench's sweep kernel (perm_sweep_units) for one
+workload on a slice of its canonical units, so `ncu --set full` replays stay short.
+
+    python tools/profile_sweep.py [--workload M4] [--fraction 64] [--alg glynn] [--reps 2]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+import paper_1606_05836_b200 as pb  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="M4")
+ap.add_argument("--fraction", type=int, default=64)
+ap.add_argument("--alg", default="glynn")
+ap.add_argument("--reps", type=int, default=2)
+a = ap.parse_args()
+A = torch.from_numpy(synth.workload(a.workload)).cuda()
+n = A.shape[0]
+alg = pb.ALG_GLYNN if a.alg == "glynn" else pb.ALG_RYSER
+P = pb.plan(n, alg)
+units = max(1, P.units // a.fraction)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for r in range(a.reps):
+    e0.record()
+    parts = pb.sweep_units(A, alg, 0, units)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    terms = units * P.unit_terms
+    print(f"n={n} alg={a.alg} units={units}/{P.units} {ms:.2f} ms {terms / ms * 1e3:.4e} terms/s "
+          f"alg {terms * (8 * n - 4) / ms / 1e9:.2f} TFLOP/s instr {terms * (6 * n - 2) / (ms * 1e-3) / (148 * 64 * 1.965e9):.3f}")
