@@ -160,8 +160,9 @@ def run_ours(args, rank, world, local_rank):
     import paper_1606_05836_b200 as pb
     from paper_1606_05836_b200 import dist as pdist
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % torch.cuda.device_count()   # ranks share a GPU only in gloo tests
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     A_np = synth.workload(args.workload)
     n = A_np.shape[0]
     alg = pb.ALG_GLYNN
@@ -200,7 +201,7 @@ def run_ours(args, rank, world, local_rank):
         v = step(False)
         flush.zero_()
     barrier()
-    clocks = ClockSampler(local_rank)
+    clocks = ClockSampler(dev_index)
     clocks.start()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -246,7 +247,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = my_terms * flop_per_term / (sweep_max * 1e-3) / 1e12
     fp64_instr_per_term = 6 * n - 2
     instr_frac = my_terms * fp64_instr_per_term / (sweep_max * 1e-3) / (SM_COUNT * FP64_FMA_PER_SM_CLK * SM_MAX_MHZ * 1e6)
-    traffic = None
+    traffic = None       # dram read+write bytes of the profiled sweep launch (profiles/traffic.json)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
@@ -270,6 +271,7 @@ def run_ours(args, rank, world, local_rank):
                             "units": P.units}},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "traffic_note": "dram bytes of the ncu --set full launch (2048 of the plan's units; profiles/)",
                      "kernel": "sweep_kernel (perm_sweep_units)", "flop_per_term": flop_per_term,
                      "fp64_instr_frac": instr_frac,
                      "peak_note": "derived FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §Roofline)"},
@@ -308,8 +310,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("PERMB200_DIST_BACKEND", "nccl")    # gloo: CPU-side test of the N>1 logic
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         return run_ours(args, rank, world, local_rank)
     finally:
