@@ -58,7 +58,12 @@ enum {
   PERM_ENOTIMPL = 3
 };
 
-enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1 };
+/* Algorithm codes.  *_DD: the double-double precision mode: the same Gray
+ * walk with every row sum, partial product and term carried as hi + lo (~2^-104 relative);
+ * about 10x the FP64 instruction count per term.  Integer matrices whose partial products
+ * and partial sums stay below 2^104 are evaluated exactly (e.g. J_20 -> 20!, J_20 - I -> D_20,
+ * both beyond one double; reading R9). */
+enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_RYSER_DD = 3 };
 
 /* The canonical evaluation plan for (n, alg).  It depends only on (n, alg), never on
  * the GPU count, so any partition of the unit range reproduces the single-GPU result
@@ -95,6 +100,14 @@ int perm_plan(int n, int alg, perm_plan_t* plan);
 int perm_glynn(const perm_c128* A, int n, perm_c128* out, void* stream);
 int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream);
 
+/* ---- double-double precision mode (device pointers) -------------------------------- */
+/* out[0] = Perm(A) as a complex double-double (re_hi, re_lo, im_hi, im_lo), already scaled by
+ * 2^{-(N-1)} (Glynn; exact).  Same plan/tree structure as the FP64 entry points with
+ * alg = PERM_ALG_GLYNN_DD / PERM_ALG_RYSER_DD.  A: device, n*n; out: device, 1 element.
+ * Zero components are +0 in both halves.  PERM_EINVAL as perm_glynn / perm_ryser. */
+int perm_glynn_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream);
+int perm_ryser_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream);
+
 /* ---- building blocks for multi-GPU partitions --------------------------------------- */
 /* Sweep kernel only: unit partials for units [unit_lo, unit_hi) of plan(n, alg), written
  * to unit_partials[0 .. unit_hi-unit_lo) (device).  One kernel launch (plus a tiny
@@ -107,6 +120,8 @@ int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_
  * power-of-two block of units, the value equals that node of the canonical tree. */
 int perm_glynn_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream);
 int perm_ryser_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream);
+/* The same for any algorithm code (FP64 or double-double). */
+int perm_range(const perm_c128* A, int n, int alg, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream);
 
 /* Canonical pairwise tree over `count` partials (device; zero-padded to a power of two:
  * node = left + right in double-double, left = lower indices).  Writes the unscaled root

@@ -8,7 +8,9 @@ on any non-zero status.  PyTorch supplies device memory and streams only.
 
     glynn(A) / ryser(A)              permanent of one n x n complex128 CUDA matrix
     glynn_batched(As)                (B, n, n) -> (B,)  one permanent per thread block
+    glynn_dd(A) / ryser_dd(A)        double-double precision mode: (re_hi, re_lo, im_hi, im_lo)
     glynn_range / ryser_range        unscaled double-double partial over Gray indices [lo, hi)
+    range_partial(A, alg, lo, hi)    the same for any algorithm code (incl. the dd mode)
     sweep_units / combine            the two kernels of the canonical reduction (multi-GPU)
     glynn_host / ryser_host / glynn_batched_host   host-buffer C-ABI entry points
     dist.perm_dist                   one permanent partitioned over a process group (NCCL)
@@ -20,11 +22,12 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import ALG_GLYNN, ALG_RYSER, Plan, PermError, max_n, plan  # noqa: F401
+from ._lib import ALG_GLYNN, ALG_GLYNN_DD, ALG_RYSER, ALG_RYSER_DD, Plan, PermError, max_n, plan  # noqa: F401
 
 __all__ = ["glynn", "ryser", "glynn_batched", "glynn_range", "ryser_range", "sweep_units", "combine",
            "glynn_host", "ryser_host", "glynn_batched_host", "plan", "max_n", "Plan", "PermError",
-           "ALG_GLYNN", "ALG_RYSER"]
+           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "glynn_dd", "ryser_dd", "range_partial",
+           "dd_to_complex"]
 
 
 def _stream(device: torch.device) -> int:
@@ -44,6 +47,10 @@ def _alg(alg) -> int:
         return ALG_GLYNN
     if alg in (ALG_RYSER, "ryser"):
         return ALG_RYSER
+    if alg in (ALG_GLYNN_DD, "glynn_dd"):
+        return ALG_GLYNN_DD
+    if alg in (ALG_RYSER_DD, "ryser_dd"):
+        return ALG_RYSER_DD
     raise ValueError(f"unknown algorithm {alg!r}")
 
 
@@ -64,6 +71,32 @@ def glynn(A: torch.Tensor) -> torch.Tensor:
 def ryser(A: torch.Tensor) -> torch.Tensor:
     """Perm(A) by Ryser, Eq. (1)."""
     return _perm(_lib.lib().perm_ryser, "perm_ryser", A)
+
+
+def _perm_dd(fn, name: str, A: torch.Tensor) -> torch.Tensor:
+    n = _square(A)
+    A = A.contiguous()
+    out = torch.empty(4, dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(fn(A.data_ptr(), n, out.data_ptr(), _stream(A.device)), name)
+    return out
+
+
+def glynn_dd(A: torch.Tensor) -> torch.Tensor:
+    """Perm(A) by Eq. (2) in the double-double mode: (4,) float64 (re_hi, re_lo, im_hi, im_lo),
+    scaled by 2^-(n-1)."""
+    return _perm_dd(_lib.lib().perm_glynn_dd, "perm_glynn_dd", A)
+
+
+def ryser_dd(A: torch.Tensor) -> torch.Tensor:
+    """Perm(A) by Eq. (1) in the double-double mode (4 float64, see glynn_dd)."""
+    return _perm_dd(_lib.lib().perm_ryser_dd, "perm_ryser_dd", A)
+
+
+def dd_to_complex(d) -> complex:
+    """(re_hi, re_lo, im_hi, im_lo) -> complex128 (rounded)."""
+    v = [float(x) for x in (d.tolist() if hasattr(d, "tolist") else d)]
+    return complex(v[0] + v[1], v[2] + v[3])
 
 
 def glynn_batched(As: torch.Tensor) -> torch.Tensor:
@@ -98,6 +131,17 @@ def glynn_range(A: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
 def ryser_range(A: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
     """Signed Ryser partial over Gray indices [lo, hi) (double-double, 4 float64)."""
     return _range(_lib.lib().perm_ryser_range, "perm_ryser_range", A, lo, hi)
+
+
+def range_partial(A: torch.Tensor, alg, lo: int, hi: int) -> torch.Tensor:
+    """Unscaled partial over Gray indices [lo, hi) for any algorithm code (4 float64)."""
+    n = _square(A)
+    A = A.contiguous()
+    out = torch.empty(4, dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(_lib.lib().perm_range(A.data_ptr(), n, _alg(alg), int(lo), int(hi), out.data_ptr(),
+                                         _stream(A.device)), "perm_range")
+    return out
 
 
 def sweep_units(A: torch.Tensor, alg, unit_lo: int, unit_hi: int) -> torch.Tensor:

@@ -12,13 +12,13 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpermb200.so")
 
 PERM_OK, PERM_EINVAL, PERM_ECUDA, PERM_ENOTIMPL = 0, 1, 2, 3
-ALG_GLYNN, ALG_RYSER = 0, 1
+ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD = 0, 1, 2, 3
 
 # every symbol include/permb200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "perm_max_n", "perm_strerror", "perm_plan", "perm_glynn", "perm_ryser", "perm_sweep_units",
     "perm_glynn_range", "perm_ryser_range", "perm_combine", "perm_glynn_batched", "perm_glynn_host",
-    "perm_ryser_host", "perm_glynn_batched_host",
+    "perm_ryser_host", "perm_glynn_batched_host", "perm_glynn_dd", "perm_ryser_dd", "perm_range",
 )
 
 
@@ -76,6 +76,9 @@ def lib() -> ctypes.CDLL:
         L.perm_ryser_range.argtypes = [vp, i32, u64, u64, vp, vp]
         L.perm_combine.argtypes = [vp, i64, i32, i32, vp, vp, vp]
         L.perm_glynn_batched.argtypes = [vp, i32, i64, vp, vp]
+        L.perm_glynn_dd.argtypes = [vp, i32, vp, vp]
+        L.perm_ryser_dd.argtypes = [vp, i32, vp, vp]
+        L.perm_range.argtypes = [vp, i32, i32, u64, u64, vp, vp]
         L.perm_glynn_host.argtypes = [vp, i32, vp]
         L.perm_ryser_host.argtypes = [vp, i32, vp]
         L.perm_glynn_batched_host.argtypes = [vp, i32, i64, vp]

@@ -39,7 +39,7 @@ struct DeviceSlots {
 DeviceSlots g_slots[64];
 
 std::once_flag g_tables_once;
-SweepLauncher g_sweep[2][kNMax + 1];
+SweepLauncher g_sweep[4][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -52,6 +52,10 @@ void init_tables() {
     register_ryser_b(g_sweep[kRyser]);
     register_ryser_c(g_sweep[kRyser]);
     register_ryser_d(g_sweep[kRyser]);
+    register_dd_glynn_a(g_sweep[PERM_ALG_GLYNN_DD]);
+    register_dd_glynn_b(g_sweep[PERM_ALG_GLYNN_DD]);
+    register_dd_ryser_a(g_sweep[PERM_ALG_RYSER_DD]);
+    register_dd_ryser_b(g_sweep[PERM_ALG_RYSER_DD]);
     register_batched_a(g_batched);
     register_batched_b(g_batched);
   });
@@ -63,13 +67,20 @@ int ceil_log2(long long v) {
   return k;
 }
 
+bool valid_alg(int alg) { return alg >= PERM_ALG_GLYNN && alg <= PERM_ALG_RYSER_DD; }
+bool is_glynn(int alg) { return alg == PERM_ALG_GLYNN || alg == PERM_ALG_GLYNN_DD; }
+bool is_dd(int alg) { return alg == PERM_ALG_GLYNN_DD || alg == PERM_ALG_RYSER_DD; }
+
 void make_plan(int n, int alg, perm_plan_t* p) {
-  const int m = (alg == PERM_ALG_GLYNN) ? n - 1 : n;
+  const int m = is_glynn(alg) ? n - 1 : n;
+  // FP64 sweep: up to 128 threads per unit (row sums in registers); dd sweep: up to 64
+  // (row sums in shared memory, 32 B per row per thread).
+  const int wmax = is_dd(alg) ? 6 : 7;
   int wbits, c, ubits, lam;
   if (m < 5) {
     wbits = 0; c = m; ubits = 0; lam = 0;      // tiny: one thread, generic walk
   } else {
-    wbits = m - 5 < 7 ? m - 5 : 7;
+    wbits = m - 5 < wmax ? m - 5 : wmax;
     const int rem = m - wbits;
     int ct = ceil_log2(33LL * n);              // chunk build <= ~1% of the sweep's FP64 ops
     if (ct < 5) ct = 5;
@@ -89,13 +100,13 @@ void make_plan(int n, int alg, perm_plan_t* p) {
 
 bool valid_n(int n) { return n >= 1 && n <= kNMax; }
 // Ryser has 2^n terms: n = 64 would overflow the 64-bit Gray index.
-bool valid_n_alg(int n, int alg) { return valid_n(n) && (alg == PERM_ALG_GLYNN ? true : n <= 63); }
+bool valid_n_alg(int n, int alg) { return valid_alg(alg) && valid_n(n) && (is_glynn(alg) ? true : n <= 63); }
 
 // Canonical tree over `count` partials (zero-padded to P = 2^k): one block of up to 1024
 // threads; thread t reduces the aligned segment [t*S, (t+1)*S) with the binary-counter
 // method (node = left + right), then a pairwise tree over the segment roots in smem.
 __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int64_t P, int do_scale,
-                               int scale_exp, double2* out, Dd2* out_dd) {
+                               int scale_exp, double2* out, Dd2* out_dd, int scale_dd) {
   __shared__ Dd2 red[1024];
   const int64_t T = P < 1024 ? P : 1024;
   const int64_t S = P / T;
@@ -120,9 +131,18 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
   }
   if (tid == 0) {
     const Dd2 r = red[0];
-    if (out_dd) *out_dd = r;
+    const int e = do_scale ? scale_exp : 0;
+    if (out_dd) {
+      Dd2 o = r;
+      if (scale_dd) {            // exact power-of-two scaling of both halves
+        o.re_hi = ldexp(o.re_hi, e); o.re_lo = ldexp(o.re_lo, e);
+        o.im_hi = ldexp(o.im_hi, e); o.im_lo = ldexp(o.im_lo, e);
+        if (o.re_hi == 0.0) { o.re_hi = 0.0; o.re_lo = 0.0; }   // canonical +0 (reading R11)
+        if (o.im_hi == 0.0) { o.im_hi = 0.0; o.im_lo = 0.0; }
+      }
+      *out_dd = o;
+    }
     if (out) {
-      const int e = do_scale ? scale_exp : 0;
       double re = __dadd_rn(ldexp(r.re_hi, e), ldexp(r.re_lo, e));
       double im = __dadd_rn(ldexp(r.im_hi, e), ldexp(r.im_lo, e));
       if (re == 0.0) re = 0.0;   // canonical +0 (reading R11)
@@ -132,10 +152,11 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
   }
 }
 
-int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, Dd2* out_dd, cudaStream_t st) {
+int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, Dd2* out_dd, cudaStream_t st,
+                int scale_dd = 0) {
   int64_t P = 1;
   while (P < count) P <<= 1;
-  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, alg == PERM_ALG_GLYNN, -(n - 1), out, out_dd);
+  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, is_glynn(alg), -(n - 1), out, out_dd, scale_dd);
   CUDA_TRY(cudaGetLastError(), "combine_kernel launch");
   return PERM_OK;
 }
@@ -154,6 +175,11 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   a.unit_lo = u_lo;
   a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
   a.zero = 0;
+  if (is_dd(P.alg)) {            // the dd sweep reads its columns from A: no constant slot
+    a.slot = 0; a.col_base = 0;
+    CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "dd sweep launch");
+    return PERM_OK;
+  }
   DeviceSlots& ds = g_slots[dev];
   std::lock_guard<std::mutex> lk(ds.mu);
   if (!ds.init) {
@@ -174,8 +200,9 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
 
 constexpr size_t kStagingBytes = sizeof(double2) * kTabRows * kNMax;
 
-int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t st) {
-  if (!A || !out || !valid_n_alg(n, alg)) return PERM_EINVAL;
+// out (complex128) and/or out_dd (scaled double-double) of the full permanent.
+int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t st, perm_dd_c128* out_dd = nullptr) {
+  if (!A || (!out && !out_dd) || !valid_n_alg(n, alg)) return PERM_EINVAL;
   perm_plan_t P;
   make_plan(n, alg, &P);
   void* ws = nullptr;
@@ -185,7 +212,8 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
   Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
   const uint64_t T = 1ULL << P.log2_terms;
   int rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
-  if (rc == PERM_OK) rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), nullptr, st);
+  if (rc == PERM_OK)
+    rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), st, 1);
   cudaError_t e = cudaFreeAsync(ws, st);
   if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
   return rc;
@@ -241,7 +269,7 @@ const char* perm_strerror(int code) {
 }
 
 int perm_plan(int n, int alg, perm_plan_t* plan) {
-  if (!plan || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
+  if (!plan || !valid_n_alg(n, alg)) return PERM_EINVAL;
   make_plan(n, alg, plan);
   return PERM_OK;
 }
@@ -254,9 +282,23 @@ int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream) {
   return full_perm(A, n, PERM_ALG_RYSER, out, static_cast<cudaStream_t>(stream));
 }
 
+int perm_glynn_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream) {
+  if (!out) return PERM_EINVAL;
+  return full_perm(A, n, PERM_ALG_GLYNN_DD, nullptr, static_cast<cudaStream_t>(stream), out);
+}
+
+int perm_ryser_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream) {
+  if (!out) return PERM_EINVAL;
+  return full_perm(A, n, PERM_ALG_RYSER_DD, nullptr, static_cast<cudaStream_t>(stream), out);
+}
+
+int perm_range(const perm_c128* A, int n, int alg, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream) {
+  return range_perm(A, n, alg, lo, hi, partial, static_cast<cudaStream_t>(stream));
+}
+
 int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_t unit_hi,
                      perm_dd_c128* unit_partials, void* stream) {
-  if (!A || !unit_partials || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
+  if (!A || !unit_partials || !valid_n_alg(n, alg)) return PERM_EINVAL;
   perm_plan_t P;
   make_plan(n, alg, &P);
   if (unit_lo < 0 || unit_lo > unit_hi || unit_hi > P.units) return PERM_EINVAL;
@@ -281,7 +323,7 @@ int perm_ryser_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_d
 
 int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg, perm_c128* out,
                  perm_dd_c128* out_dd, void* stream) {
-  if (!partials || count < 1 || (alg != PERM_ALG_GLYNN && alg != PERM_ALG_RYSER) || !valid_n_alg(n, alg)) return PERM_EINVAL;
+  if (!partials || count < 1 || !valid_n_alg(n, alg)) return PERM_EINVAL;
   if (!out && !out_dd) return PERM_EINVAL;
   return run_combine(reinterpret_cast<const Dd2*>(partials), count, n, alg, reinterpret_cast<double2*>(out),
                      reinterpret_cast<Dd2*>(out_dd), static_cast<cudaStream_t>(stream));

@@ -102,11 +102,21 @@ __device__ __forceinline__ Dd2 dd2_add(const Dd2& a, const Dd2& b) {
   return r;
 }
 
-// Product of the n row sums: 4 independent chains (i mod 4) then a pairwise tree.
+// Number of independent product chains for n.  4 gives the most ILP, but near the 255-register
+// cap (4n registers of row sums) ptxas's allocation of the half-walk loop is erratic: per n, the
+// chain count below is the one whose loop has no local-memory spills and the fewest register
+// moves in the SASS (tools/sass_loop_stats.py, 2026-10-19: n = 50 with 4 chains spilled 28
+// accesses and moved 205 registers per 4 terms; with 3 chains: 0 spills, 32 moves).  Beyond
+// n = 53 every count spills; 2 is the least bad.
+__host__ __device__ constexpr int product_chains(int N) {
+  return N < 4 ? N : (N == 49 || N >= 54) ? 2 : (N == 50 || N == 53) ? 3 : 4;
+}
+
+// Product of the n row sums: NC independent chains (i mod NC) then a pairwise tree.
 // The order depends only on N, so every kernel/launch shape computes identical terms.
 template <int N>
 __device__ __forceinline__ double2 row_product(const double2 (&s)[N]) {
-  constexpr int NC = N < 4 ? N : 4;
+  constexpr int NC = product_chains(N);
   double2 c[NC];
 #pragma unroll
   for (int k = 0; k < NC; ++k) c[k] = s[k];
@@ -323,6 +333,19 @@ __device__ __noinline__ Dd2 chunk_generic(const double2* __restrict__ at, uint64
   return w.result();
 }
 
+// Chunks k in [k0, k1) of leaf `leaf_id` (chunks q = leaf_id 2^lam + k of 2^c Gray indices)
+// that intersect [lo, hi): a ragged range touching a few chunks of a long leaf (large n:
+// 2^27 chunks per leaf) must not iterate over the rest.
+__device__ __forceinline__ void leaf_chunk_window(uint64_t leaf_id, int c, int lam, uint64_t lo, uint64_t hi,
+                                                  uint64_t& k0, uint64_t& k1) {
+  const uint64_t first = leaf_id << lam, nchunks = 1ull << lam;
+  const uint64_t qlo = lo >> c, qhi = (hi + (1ull << c) - 1) >> c;     // chunks [qlo, qhi) meet [lo, hi)
+  k0 = qlo > first ? qlo - first : 0;
+  k1 = qhi > first ? qhi - first : 0;
+  if (k0 > nchunks) k0 = nchunks;
+  if (k1 > nchunks) k1 = nchunks;
+}
+
 // One leaf = 2^lam consecutive chunks walked in order by one thread; chunk partials are
 // combined in order with double-double additions.  kFast: every chunk lies inside the
 // range and c >= 5 (decided by the caller from block-uniform values).
@@ -330,8 +353,11 @@ template <int N, int ALG, bool kFast, class Cols>
 __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
                                          int c, int lam, uint64_t lo, uint64_t hi, int zero) {
   Dd2 acc{0.0, 0.0, 0.0, 0.0};
-  const uint64_t nchunks = 1ull << lam;
-  for (uint64_t k = 0; k < nchunks; ++k) {
+  // Fast path: all 2^lam chunks (this exact loop shape keeps ptxas's uniform-register column
+  // path, tests/test_build_sass.py).  Ragged path: only chunks [k0, k1) meeting [lo, hi).
+  uint64_t k0 = 0, k1 = 1ull << lam;
+  if (!kFast) leaf_chunk_window(leaf_id, c, lam, lo, hi, k0, k1);
+  for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t q = (leaf_id << lam) + k;
     if (kFast) {
       acc = dd2_add(acc, chunk_fast<N, ALG>(cols, at, q, c, zero));

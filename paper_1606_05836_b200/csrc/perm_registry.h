@@ -11,6 +11,10 @@ void register_ryser_a(SweepLauncher* t);
 void register_ryser_b(SweepLauncher* t);
 void register_ryser_c(SweepLauncher* t);
 void register_ryser_d(SweepLauncher* t);
+void register_dd_glynn_a(SweepLauncher* t);
+void register_dd_glynn_b(SweepLauncher* t);
+void register_dd_ryser_a(SweepLauncher* t);
+void register_dd_ryser_b(SweepLauncher* t);
 void register_batched_a(BatchedLauncher* t);
 void register_batched_b(BatchedLauncher* t);
 }  // namespace permb200
