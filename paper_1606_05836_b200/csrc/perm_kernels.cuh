@@ -423,8 +423,15 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) 
 // Batched Glynn: block b computes Perm(A_b) completely (boson sampling needs
 // many permanents of n x n submatrices).  Columns come from the block's shared-memory copy
 // (warp-uniform addresses: broadcast LDS).
+// Resident blocks per SM the batched kernel is compiled for: the shared-memory column operands
+// are loaded into vector registers, so ptxas's default allocation (n = 16: 168 registers, 3
+// blocks/SM, 9.2 waves for M2's 4096 permanents; ncu profiles/r01_batched_m2_*) leaves warps
+// idle.  At 4 blocks (<= 128 registers) chunk_fast<16> still has no spills (only the kernel
+// body spills a few values across the chunk call).
+__host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? 4 : N <= 20 ? 3 : 1; }
+
 template <int N>
-__global__ void __launch_bounds__(kMaxBlock) batched_kernel(const BatchedArgs args) {
+__global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kernel(const BatchedArgs args) {
   extern __shared__ double2 smem[];
   double2* at = smem;
   double2* tab = smem + N * N;

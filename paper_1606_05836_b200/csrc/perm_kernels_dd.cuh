@@ -72,19 +72,27 @@ __device__ __forceinline__ cdd cmul(const cdd& a, const cdd& b) {
   return r;
 }
 
+// Independent product chains (i mod kDdChains): the dd multiply is a ~22-deep dependent
+// chain per component, and shared-memory residency limits a block to 2 warps, so the
+// chains are what hides the FP64 latency (ncu r01_dd_n32: "wait" stalls dominate).
+constexpr int kDdChains = 4;
+// Stride (in double2) between a thread's consecutive row-sum slots = the largest dd block.
+// A compile-time stride lets the compiler prove that the store of row i and the load of row
+// i+1 do not alias, so the rows' independent update chains interleave.
+constexpr int kDdStride = 64;
+
 template <int N, int ALG>
 struct DdWalker {
-  double2* ss;       // this thread's row sums: element (i, part) at ss[(2 i + part) * T]
-  int T;
+  double2* ss;       // this thread's row sums: element (i, part) at ss[(2 i + part) * kDdStride]
   dd ar, ai;         // term accumulator
 
   __device__ __forceinline__ cdd load(int i) const {
-    const double2 r = ss[(2 * i) * T], m = ss[(2 * i + 1) * T];
+    const double2 r = ss[(2 * i) * kDdStride], m = ss[(2 * i + 1) * kDdStride];
     return cdd{dd{r.x, r.y}, dd{m.x, m.y}};
   }
   __device__ __forceinline__ void store(int i, const cdd& v) {
-    ss[(2 * i) * T] = make_double2(v.re.hi, v.re.lo);
-    ss[(2 * i + 1) * T] = make_double2(v.im.hi, v.im.lo);
+    ss[(2 * i) * kDdStride] = make_double2(v.re.hi, v.re.lo);
+    ss[(2 * i + 1) * kDdStride] = make_double2(v.im.hi, v.im.lo);
   }
 
   // Row sums for code G from the row-major matrix A: Glynn s_i = a_i1 +
@@ -119,8 +127,9 @@ struct DdWalker {
     ai = dd{0.0, 0.0};
     double sg = 0.0;
     int col = 0;
+    constexpr int NC = N < kDdChains ? N : kDdChains;
     for (uint64_t g = ga;;) {
-      cdd c0, c1;
+      cdd c[NC];
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         cdd s = load(i);
@@ -128,12 +137,15 @@ struct DdWalker {
         s.re = add_d(s.re, __dmul_rn(sg, v.x));
         s.im = add_d(s.im, __dmul_rn(sg, v.y));
         store(i, s);
-        if (i == 0) c0 = s;
-        else if (i == 1) c1 = s;
-        else if (i & 1) c1 = cmul(c1, s);
-        else c0 = cmul(c0, s);
+        c[i % NC] = (i < NC) ? s : cmul(c[i % NC], s);
       }
-      cdd p = (N > 1) ? cmul(c0, c1) : c0;
+      // pairwise tree over the chains (order fixed by N)
+#pragma unroll
+      for (int w = 1; w < NC; w *= 2) {
+#pragma unroll
+        for (int k = 0; k + w < NC; k += 2 * w) c[k] = cmul(c[k], c[k + w]);
+      }
+      cdd p = c[0];
       if (((g & 1) != 0) != kNegBase) {
         p.re.hi = -p.re.hi; p.re.lo = -p.re.lo; p.im.hi = -p.im.hi; p.im.lo = -p.im.lo;
       }
@@ -150,15 +162,14 @@ struct DdWalker {
 };
 
 // One block = one unit of the dd plan (perm_api.cu make_plan, block_bits <= 6); thread =
-// leaf of 2^lam chunks.  Dynamic shared memory: 2 N T double2 (row sums) + T Dd2 (tree).
+// leaf of 2^lam chunks.  Dynamic shared memory: 2 N kDdStride double2 (row sums) + blockDim
+// Dd2 (tree).
 template <int N, int ALG>
-__global__ void __launch_bounds__(64) sweep_dd_kernel(const SweepArgs args) {
+__global__ void __launch_bounds__(kDdStride) sweep_dd_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
-  const int T = blockDim.x;
-  Dd2* red = reinterpret_cast<Dd2*>(smem + 2 * N * T);
+  Dd2* red = reinterpret_cast<Dd2*>(smem + 2 * N * kDdStride);
   DdWalker<N, ALG> w;
   w.ss = smem + threadIdx.x;
-  w.T = T;
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 acc{0.0, 0.0, 0.0, 0.0};
@@ -184,7 +195,7 @@ __global__ void __launch_bounds__(64) sweep_dd_kernel(const SweepArgs args) {
 template <int N, int ALG>
 cudaError_t launch_sweep_dd(const SweepArgs& a, int64_t units, double2*, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
-  const size_t smem = sizeof(double2) * 2 * N * threads + sizeof(Dd2) * threads;
+  const size_t smem = sizeof(double2) * 2 * N * kDdStride + sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(sweep_dd_kernel<N, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

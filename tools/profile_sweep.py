@@ -1,7 +1,10 @@
-"""Profiling driver (ncu target): run the bench's sweep kernel (perm_sweep_units) for one
-workload on a slice of its canonical units, so `ncu --set full` replays stay short.
+"""Profiling driver (ncu target): run one kernel of the hot path on a slice of its canonical
+units, so `ncu --set full` replays stay short.
 
-    python tools/profile_sweep.py [--workload M4] [--fraction 64] [--alg glynn] [--reps 2]
+    python tools/profile_sweep.py [--workload M4] [--fraction 64 | --units U] [--alg glynn] [--reps 2]
+    python tools/profile_sweep.py --workload M2 --batched [--reps 2]
+
+--alg: glynn | ryser | glynn_dd | ryser_dd.  --batched times perm_glynn_batched on M2.
 """
 import argparse
 import os
@@ -18,15 +21,29 @@ import paper_1606_05836_b200 as pb  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="M4")
 ap.add_argument("--fraction", type=int, default=64)
+ap.add_argument("--units", type=int, default=0, help="sweep exactly this many units (overrides --fraction)")
 ap.add_argument("--alg", default="glynn")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--batched", action="store_true")
 a = ap.parse_args()
 A = torch.from_numpy(synth.workload(a.workload)).cuda()
-n = A.shape[0]
-alg = pb.ALG_GLYNN if a.alg == "glynn" else pb.ALG_RYSER
-P = pb.plan(n, alg)
-units = max(1, P.units // a.fraction)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+if a.batched:
+    B, n = A.shape[0], A.shape[1]
+    for r in range(a.reps):
+        e0.record()
+        pb.glynn_batched(A)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        terms = B * (1 << (n - 1))
+        print(f"batched B={B} n={n} {ms:.3f} ms {terms / ms * 1e3:.4e} terms/s "
+              f"instr {terms * (6 * n - 2) / (ms * 1e-3) / (148 * 64 * 1.965e9):.3f}")
+    sys.exit(0)
+n = A.shape[0]
+alg = pb._alg(a.alg)
+P = pb.plan(n, alg)
+units = a.units or max(1, P.units // a.fraction)
 for r in range(a.reps):
     e0.record()
     parts = pb.sweep_units(A, alg, 0, units)
