@@ -63,7 +63,12 @@ enum {
  * about 10x the FP64 instruction count per term.  Integer matrices whose partial products
  * and partial sums stay below 2^104 are evaluated exactly (e.g. J_20 -> 20!, J_20 - I -> D_20,
  * both beyond one double; reading R9). */
-enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_RYSER_DD = 3 };
+/* *_PLAIN: the FP64 sweep with every accumulation in plain (uncompensated) FP64 -- the
+ * paper's "Perm = Perm +- delta" -- for the precision lab's
+ * compensated-vs-plain accumulation discrepancy.  Same terms, same order,
+ * same speed; partials carry lo = 0 and perm_combine adds them in plain FP64. */
+enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_RYSER_DD = 3,
+       PERM_ALG_GLYNN_PLAIN = 4, PERM_ALG_RYSER_PLAIN = 5 };
 
 /* The canonical evaluation plan for (n, alg).  It depends only on (n, alg), never on
  * the GPU count, so any partition of the unit range reproduces the single-GPU result

@@ -11,6 +11,7 @@ on any non-zero status.  PyTorch supplies device memory and streams only.
     glynn_dd(A) / ryser_dd(A)        double-double precision mode: (re_hi, re_lo, im_hi, im_lo)
     glynn_range / ryser_range        unscaled double-double partial over Gray indices [lo, hi)
     range_partial(A, alg, lo, hi)    the same for any algorithm code (incl. the dd mode)
+    perm_alg(A, alg)                 Perm(A) for any algorithm code (FP64 / dd / plain accumulation)
     sweep_units / combine            the two kernels of the canonical reduction (multi-GPU)
     glynn_host / ryser_host / glynn_batched_host   host-buffer C-ABI entry points
     dist.perm_dist                   one permanent partitioned over a process group (NCCL)
@@ -22,11 +23,12 @@ import ctypes
 import torch
 
 from . import _lib
-from ._lib import ALG_GLYNN, ALG_GLYNN_DD, ALG_RYSER, ALG_RYSER_DD, Plan, PermError, max_n, plan  # noqa: F401
+from ._lib import (ALG_GLYNN, ALG_GLYNN_DD, ALG_GLYNN_PLAIN, ALG_RYSER, ALG_RYSER_DD, ALG_RYSER_PLAIN,  # noqa: F401
+                   Plan, PermError, max_n, plan)
 
 __all__ = ["glynn", "ryser", "glynn_batched", "glynn_range", "ryser_range", "sweep_units", "combine",
            "glynn_host", "ryser_host", "glynn_batched_host", "plan", "max_n", "Plan", "PermError",
-           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "glynn_dd", "ryser_dd", "range_partial",
+           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "ALG_GLYNN_PLAIN", "ALG_RYSER_PLAIN", "glynn_dd", "ryser_dd", "range_partial", "perm_alg",
            "dd_to_complex"]
 
 
@@ -51,6 +53,10 @@ def _alg(alg) -> int:
         return ALG_GLYNN_DD
     if alg in (ALG_RYSER_DD, "ryser_dd"):
         return ALG_RYSER_DD
+    if alg in (ALG_GLYNN_PLAIN, "glynn_plain"):
+        return ALG_GLYNN_PLAIN
+    if alg in (ALG_RYSER_PLAIN, "ryser_plain"):
+        return ALG_RYSER_PLAIN
     raise ValueError(f"unknown algorithm {alg!r}")
 
 
@@ -142,6 +148,16 @@ def range_partial(A: torch.Tensor, alg, lo: int, hi: int) -> torch.Tensor:
         _lib.check(_lib.lib().perm_range(A.data_ptr(), n, _alg(alg), int(lo), int(hi), out.data_ptr(),
                                          _stream(A.device)), "perm_range")
     return out
+
+
+def perm_alg(A: torch.Tensor, alg) -> torch.Tensor:
+    """Perm(A) for any algorithm code (FP64, double-double or plain-accumulation mode),
+    rounded to a 0-d complex128 tensor: sweep_units over all units + combine (one call each)."""
+    n = _square(A)
+    a = _alg(alg)
+    P = plan(n, a)
+    val, _ = combine(sweep_units(A, a, 0, P.units), n, a, scale=True)
+    return val
 
 
 def sweep_units(A: torch.Tensor, alg, unit_lo: int, unit_hi: int) -> torch.Tensor:

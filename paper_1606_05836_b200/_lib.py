@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpermb200.so")
 
 PERM_OK, PERM_EINVAL, PERM_ECUDA, PERM_ENOTIMPL = 0, 1, 2, 3
-ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD = 0, 1, 2, 3
+ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD, ALG_GLYNN_PLAIN, ALG_RYSER_PLAIN = 0, 1, 2, 3, 4, 5
 
 # every symbol include/permb200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

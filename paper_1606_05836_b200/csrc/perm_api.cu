@@ -39,7 +39,7 @@ struct DeviceSlots {
 DeviceSlots g_slots[64];
 
 std::once_flag g_tables_once;
-SweepLauncher g_sweep[4][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD
+SweepLauncher g_sweep[6][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -52,6 +52,14 @@ void init_tables() {
     register_ryser_b(g_sweep[kRyser]);
     register_ryser_c(g_sweep[kRyser]);
     register_ryser_d(g_sweep[kRyser]);
+    register_plain_glynn_a(g_sweep[PERM_ALG_GLYNN_PLAIN]);
+    register_plain_glynn_b(g_sweep[PERM_ALG_GLYNN_PLAIN]);
+    register_plain_glynn_c(g_sweep[PERM_ALG_GLYNN_PLAIN]);
+    register_plain_glynn_d(g_sweep[PERM_ALG_GLYNN_PLAIN]);
+    register_plain_ryser_a(g_sweep[PERM_ALG_RYSER_PLAIN]);
+    register_plain_ryser_b(g_sweep[PERM_ALG_RYSER_PLAIN]);
+    register_plain_ryser_c(g_sweep[PERM_ALG_RYSER_PLAIN]);
+    register_plain_ryser_d(g_sweep[PERM_ALG_RYSER_PLAIN]);
     register_dd_glynn_a(g_sweep[PERM_ALG_GLYNN_DD]);
     register_dd_glynn_b(g_sweep[PERM_ALG_GLYNN_DD]);
     register_dd_ryser_a(g_sweep[PERM_ALG_RYSER_DD]);
@@ -67,8 +75,10 @@ int ceil_log2(long long v) {
   return k;
 }
 
-bool valid_alg(int alg) { return alg >= PERM_ALG_GLYNN && alg <= PERM_ALG_RYSER_DD; }
-bool is_glynn(int alg) { return alg == PERM_ALG_GLYNN || alg == PERM_ALG_GLYNN_DD; }
+bool valid_alg(int alg) { return alg >= PERM_ALG_GLYNN && alg <= PERM_ALG_RYSER_PLAIN; }
+// alg = formula (bit 0: 0 Glynn, 1 Ryser) + 2 * arithmetic mode (0 FP64, 1 dd, 2 plain FP64)
+bool is_glynn(int alg) { return (alg & 1) == 0; }
+bool is_plain(int alg) { return alg == PERM_ALG_GLYNN_PLAIN || alg == PERM_ALG_RYSER_PLAIN; }
 bool is_dd(int alg) { return alg == PERM_ALG_GLYNN_DD || alg == PERM_ALG_RYSER_DD; }
 
 void make_plan(int n, int alg, perm_plan_t* p) {
@@ -106,7 +116,7 @@ bool valid_n_alg(int n, int alg) { return valid_alg(alg) && valid_n(n) && (is_gl
 // threads; thread t reduces the aligned segment [t*S, (t+1)*S) with the binary-counter
 // method (node = left + right), then a pairwise tree over the segment roots in smem.
 __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int64_t P, int do_scale,
-                               int scale_exp, double2* out, Dd2* out_dd, int scale_dd) {
+                               int scale_exp, double2* out, Dd2* out_dd, int scale_dd, int plain) {
   __shared__ Dd2 red[1024];
   const int64_t T = P < 1024 ? P : 1024;
   const int64_t S = P / T;
@@ -118,7 +128,7 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
       const int64_t idx = tid * S + k;
       Dd2 v = idx < count ? parts[idx] : Dd2{0.0, 0.0, 0.0, 0.0};
       int lvl = 0;
-      for (int64_t kk = k; kk & 1; kk >>= 1) { v = dd2_add(stack[lvl], v); ++lvl; }
+      for (int64_t kk = k; kk & 1; kk >>= 1) { v = plain ? plain2_add(stack[lvl], v) : dd2_add(stack[lvl], v); ++lvl; }
       stack[lvl] = v;
       if (lvl > top_level) top_level = lvl;
     }
@@ -126,7 +136,8 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
   }
   __syncthreads();
   for (int64_t o = 1; o < T; o <<= 1) {
-    if ((tid & (2 * o - 1)) == 0 && tid + o < T) red[tid] = dd2_add(red[tid], red[tid + o]);
+    if ((tid & (2 * o - 1)) == 0 && tid + o < T)
+      red[tid] = plain ? plain2_add(red[tid], red[tid + o]) : dd2_add(red[tid], red[tid + o]);
     __syncthreads();
   }
   if (tid == 0) {
@@ -156,7 +167,7 @@ int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, D
                 int scale_dd = 0) {
   int64_t P = 1;
   while (P < count) P <<= 1;
-  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, is_glynn(alg), -(n - 1), out, out_dd, scale_dd);
+  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, is_glynn(alg), -(n - 1), out, out_dd, scale_dd, is_plain(alg));
   CUDA_TRY(cudaGetLastError(), "combine_kernel launch");
   return PERM_OK;
 }

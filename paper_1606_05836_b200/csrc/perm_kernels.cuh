@@ -152,11 +152,26 @@ struct SmemColumns {
   __device__ __forceinline__ double2 get(int row, int i) const { return tab[row * N + i]; }
 };
 
+// Plain (uncompensated) FP64 addition of two partials: the paper's accumulation
+// ("Perm = Perm +- delta"; reading R12) used by the PLAIN mode; only the hi
+// halves are used, lo stays 0.
+__device__ __forceinline__ Dd2 plain2_add(const Dd2& a, const Dd2& b) {
+  return Dd2{__dadd_rn(a.re_hi, b.re_hi), 0.0, __dadd_rn(a.im_hi, b.im_hi), 0.0};
+}
+
+template <bool PLAIN>
+__device__ __forceinline__ Dd2 part_add(const Dd2& a, const Dd2& b) {
+  return PLAIN ? plain2_add(a, b) : dd2_add(a, b);
+}
+
 // ------------------------------------------------------------------ the walker
-template <int N, int ALG>
+// PLAIN = false: compensated accumulation (Sum2 cascade + dd partials, the default);
+// PLAIN = true: every accumulation in plain FP64 (the precision lab's "plain" mode, §8(f)2:
+// same terms, same order, only the compensation removed).
+template <int N, int ALG, bool PLAIN = false>
 struct Walker {
   double2 s[N];                  // row sums (registers)
-  double arh, arl, aih, ail;     // cascaded (Sum2) double-double accumulators
+  double arh, arl, aih, ail;     // cascaded (Sum2) double-double accumulators (PLAIN: arh, aih only)
 
   // Column sources hold STEP VECTORS u = kScale * column (Glynn 2a: exact doubling; Ryser a).
   // Direction bit d of a flip: Glynn d=1 -> delta back to +1 -> +u, d=0 -> delta to -1 -> -u;
@@ -170,6 +185,11 @@ struct Walker {
   __device__ __forceinline__ void zero_acc() { arh = arl = aih = ail = 0.0; }
 
   __device__ __forceinline__ void acc_add(double re, double im) {
+    if (PLAIN) {
+      arh = __dadd_rn(arh, re);
+      aih = __dadd_rn(aih, im);
+      return;
+    }
     double s_, e_;
     two_sum(arh, re, s_, e_);
     arh = s_; arl = __dadd_rn(arl, e_);
@@ -305,6 +325,7 @@ struct Walker {
   }
 
   __device__ __forceinline__ Dd2 result() const {
+    if (PLAIN) return Dd2{arh, 0.0, aih, 0.0};
     Dd2 r;
     fast_two_sum(arh, arl, r.re_hi, r.re_lo);
     fast_two_sum(aih, ail, r.im_hi, r.im_lo);
@@ -316,18 +337,18 @@ struct Walker {
 // in a separate ptxas allocation unit is what lets ptxas hold the half-walk loop counter in
 // a uniform register and feed the column operands from LDCU; inlined into the leaf loop
 // (a loop nest with the build's loop) it fell back to per-thread LDC and spilled.
-template <int N, int ALG, class Cols>
+template <int N, int ALG, bool PLAIN, class Cols>
 __device__ __noinline__ Dd2 chunk_fast(const Cols cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
-  Walker<N, ALG> w;
+  Walker<N, ALG, PLAIN> w;
   w.zero_acc();
   w.fast_chunk(cols, at, q, c, zero);
   return w.result();
 }
 
 // Ragged piece [ga, gb) of one chunk (range ends, tiny n).
-template <int N, int ALG>
+template <int N, int ALG, bool PLAIN>
 __device__ __noinline__ Dd2 chunk_generic(const double2* __restrict__ at, uint64_t ga, uint64_t gb) {
-  Walker<N, ALG> w;
+  Walker<N, ALG, PLAIN> w;
   w.zero_acc();
   w.generic_walk(at, ga, gb);
   return w.result();
@@ -349,7 +370,7 @@ __device__ __forceinline__ void leaf_chunk_window(uint64_t leaf_id, int c, int l
 // One leaf = 2^lam consecutive chunks walked in order by one thread; chunk partials are
 // combined in order with double-double additions.  kFast: every chunk lies inside the
 // range and c >= 5 (decided by the caller from block-uniform values).
-template <int N, int ALG, bool kFast, class Cols>
+template <int N, int ALG, bool kFast, bool PLAIN, class Cols>
 __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
                                          int c, int lam, uint64_t lo, uint64_t hi, int zero) {
   Dd2 acc{0.0, 0.0, 0.0, 0.0};
@@ -360,12 +381,12 @@ __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __rest
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t q = (leaf_id << lam) + k;
     if (kFast) {
-      acc = dd2_add(acc, chunk_fast<N, ALG>(cols, at, q, c, zero));
+      acc = part_add<PLAIN>(acc, chunk_fast<N, ALG, PLAIN>(cols, at, q, c, zero));
     } else {
       const uint64_t g0 = q << c, g1 = g0 + (1ull << c);
       const uint64_t ga = g0 > lo ? g0 : lo;
       const uint64_t gb = g1 < hi ? g1 : hi;
-      if (ga < gb) acc = dd2_add(acc, chunk_generic<N, ALG>(at, ga, gb));
+      if (ga < gb) acc = part_add<PLAIN>(acc, chunk_generic<N, ALG, PLAIN>(at, ga, gb));
     }
   }
   return acc;
@@ -386,12 +407,13 @@ __device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, 
 
 // Canonical block reduction: contiguous pairwise tree over the block's threads (leaves),
 // node = left + right in double-double.  Result valid in red[0].
+template <bool PLAIN = false>
 __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
   const int tid = threadIdx.x, nt = blockDim.x;
   red[tid] = mine;
   __syncthreads();
   for (int o = 1; o < nt; o <<= 1) {
-    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = dd2_add(red[tid], red[tid + o]);
+    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = part_add<PLAIN>(red[tid], red[tid + o]);
     __syncthreads();
   }
 }
@@ -399,7 +421,7 @@ __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
 // ------------------------------------------------------------------ kernels
 // One block = one unit of the canonical plan.  Dynamic shared memory: N*N double2
 // (transposed matrix) + blockDim Dd2 (reduction).
-template <int N, int ALG>
+template <int N, int ALG, bool PLAIN>
 __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
   double2* at = smem;
@@ -413,10 +435,10 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) 
   const int ubits = args.block_bits + args.lam + args.c;          // log2(unit terms)
   const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
   Dd2 mine;
-  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  else mine = walk_leaf<N, ALG, false>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
 
-  block_tree(red, mine);
+  block_tree<PLAIN>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
 }
 
@@ -454,8 +476,8 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
     const SmemColumns<N> cols{tab};
     const uint64_t terms = 1ull << (N - 1);
     Dd2 mine;
-    if (args.c >= 5) mine = walk_leaf<N, kGlynn, true>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
-    else mine = walk_leaf<N, kGlynn, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
+    if (args.c >= 5) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
+    else mine = walk_leaf<N, kGlynn, false, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
     block_tree(red, mine);
     if (threadIdx.x == 0) {
       const Dd2 r = red[0];
@@ -491,7 +513,7 @@ static __global__ void stage_columns_kernel(const double2* __restrict__ A, int n
 using SweepLauncher = cudaError_t (*)(const SweepArgs&, int64_t units, double2* staging, cudaStream_t);
 using BatchedLauncher = cudaError_t (*)(const BatchedArgs&, int grid, cudaStream_t);
 
-template <int N, int ALG>
+template <int N, int ALG, bool PLAIN = false>
 cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cudaStream_t st) {
   const int c_tab = a.c < kCMax ? a.c : kCMax;
   const int col0 = (ALG == kGlynn) ? 1 : 0;
@@ -506,10 +528,10 @@ cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cu
   const int threads = 1 << a.block_bits;
   const size_t smem = sizeof(double2) * N * N + sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  sweep_kernel<N, ALG><<<(unsigned)units, threads, smem, st>>>(a);
+  sweep_kernel<N, ALG, PLAIN><<<(unsigned)units, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -532,7 +554,11 @@ cudaError_t launch_batched(const BatchedArgs& a, int grid, cudaStream_t st) {
 namespace permb200 {
 template <int ALG, int LO, int... Is>
 void fill_sweep(SweepLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_sweep<LO + Is, ALG>), ...);
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, false>), ...);
+}
+template <int ALG, int LO, int... Is>
+void fill_sweep_plain(SweepLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, true>), ...);
 }
 template <int LO, int... Is>
 void fill_batched(BatchedLauncher* table, std::integer_sequence<int, Is...>) {

@@ -11,6 +11,14 @@ void register_ryser_a(SweepLauncher* t);
 void register_ryser_b(SweepLauncher* t);
 void register_ryser_c(SweepLauncher* t);
 void register_ryser_d(SweepLauncher* t);
+void register_plain_glynn_a(SweepLauncher* t);
+void register_plain_glynn_b(SweepLauncher* t);
+void register_plain_glynn_c(SweepLauncher* t);
+void register_plain_glynn_d(SweepLauncher* t);
+void register_plain_ryser_a(SweepLauncher* t);
+void register_plain_ryser_b(SweepLauncher* t);
+void register_plain_ryser_c(SweepLauncher* t);
+void register_plain_ryser_d(SweepLauncher* t);
 void register_dd_glynn_a(SweepLauncher* t);
 void register_dd_glynn_b(SweepLauncher* t);
 void register_dd_ryser_a(SweepLauncher* t);

@@ -1,4 +1,6 @@
-"""One permanent partitioned over a process group (PAPER.md Alg. A1/A2,
+"""Multi-GPU paths.
+
+One permanent partitioned over a process group (PAPER.md Alg. A1/A2,
 P:217-219 contiguous per-process ranges, P:230/P:261 one ALLREDUCE, P:262 final factor).
 
 Each rank sweeps a contiguous, aligned block of the canonical plan's units and reduces it to
@@ -54,3 +56,32 @@ def perm_dist(A: torch.Tensor, alg: str = "glynn", group=None,
     roots = gather_roots(root, world, rank, group)
     val, _ = combine(roots, n, a, scale=True)
     return val
+
+
+def batch_range(batch: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block of batch items owned by `rank`."""
+    return rank * batch // world, (rank + 1) * batch // world
+
+
+def batched_dist(As: torch.Tensor, group=None, fn: Optional[Callable] = None) -> torch.Tensor:
+    """Batched permanents sharded over the ranks of `group` (boson-sampling
+    probabilities need many independent permanents; no reduction, the items are
+    independent).  Every rank passes the same (B, n, n) complex128 batch (on its GPU); rank r
+    computes items batch_range(B, world, r) with perm_glynn_batched and ONE all_gather returns
+    the (B,) permanents on every rank.  `fn` defaults to the CUDA kernel."""
+    import paper_1606_05836_b200 as pb
+    fn = fn or pb.glynn_batched
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    B = As.shape[0]
+    lo, hi = batch_range(B, world, rank)
+    mine = fn(As[lo:hi])
+    if world == 1:
+        return mine
+    per = (B + world - 1) // world                      # equal-size slots for all_gather
+    buf = torch.zeros((per, 2), dtype=torch.float64, device=mine.device)
+    buf[: hi - lo] = torch.view_as_real(mine)
+    out = torch.empty((world * per, 2), dtype=torch.float64, device=mine.device)
+    dist.all_gather_into_tensor(out, buf, group=group)
+    parts = [out[r * per: r * per + batch_range(B, world, r)[1] - batch_range(B, world, r)[0]] for r in range(world)]
+    return torch.view_as_complex(torch.cat(parts).contiguous())

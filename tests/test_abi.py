@@ -44,9 +44,10 @@ def test_invalid_arguments_rejected_without_cuda():
     assert L.perm_glynn_batched(None, 4, 0, None, None) == _lib.PERM_OK     # empty batch: no-op
     assert L.perm_glynn_range(buf, 4, 5, 4, buf, None) == _lib.PERM_EINVAL   # lo > hi
     assert L.perm_glynn_range(buf, 4, 0, 9, buf, None) == _lib.PERM_EINVAL   # hi > 2^(n-1)
-    assert L.perm_sweep_units(buf, 4, 4, 0, 1, buf, None) == _lib.PERM_EINVAL  # bad alg
+    assert L.perm_sweep_units(buf, 4, 6, 0, 1, buf, None) == _lib.PERM_EINVAL  # bad alg
     assert L.perm_sweep_units(buf, 4, -1, 0, 1, buf, None) == _lib.PERM_EINVAL
-    assert L.perm_range(buf, 4, 4, 0, 1, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_range(buf, 4, 6, 0, 1, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_range(buf, 4, pb.ALG_RYSER_PLAIN, 0, 17, buf, None) == _lib.PERM_EINVAL
     assert L.perm_range(buf, 4, pb.ALG_RYSER_DD, 0, 17, buf, None) == _lib.PERM_EINVAL   # hi > 2^n
     assert L.perm_glynn_dd(None, 4, buf, None) == _lib.PERM_EINVAL
     assert L.perm_glynn_dd(buf, 4, None, None) == _lib.PERM_EINVAL
@@ -59,19 +60,28 @@ def test_invalid_arguments_rejected_without_cuda():
         pb.plan(64, pb.ALG_RYSER)                       # 2^64 Gray indices do not fit
 
 
-@pytest.mark.parametrize("alg", [pb.ALG_GLYNN, pb.ALG_RYSER, pb.ALG_GLYNN_DD, pb.ALG_RYSER_DD])
+@pytest.mark.parametrize("alg", [pb.ALG_GLYNN, pb.ALG_RYSER, pb.ALG_GLYNN_DD, pb.ALG_RYSER_DD,
+                                 pb.ALG_GLYNN_PLAIN, pb.ALG_RYSER_PLAIN])
 def test_plan_is_a_partition(alg):
-    glynn = alg in (pb.ALG_GLYNN, pb.ALG_GLYNN_DD)
+    glynn = alg % 2 == 0
     for n in range(1, 65 if glynn else 64):
         P = pb.plan(n, alg)
         m = n - 1 if glynn else n
         assert P.log2_terms == m
         assert P.chunk_bits + P.leaf_bits + P.block_bits + P.unit_bits == m
         assert P.units * P.unit_terms == 1 << m
-        assert 0 <= P.block_bits <= (7 if alg < 2 else 6) and 0 <= P.chunk_bits <= 12
+        assert 0 <= P.block_bits <= (6 if alg in (pb.ALG_GLYNN_DD, pb.ALG_RYSER_DD) else 7) and 0 <= P.chunk_bits <= 12
         if m >= 5:
             assert P.chunk_bits >= 5                       # fast path usable
         assert P.units <= 1 << 17
+
+
+def test_plain_mode_plans_equal_fp64_plans():
+    """The plain-accumulation mode walks exactly the FP64 plan (same terms, same order)."""
+    for n in (5, 20, 40, 50):
+        for a, p in ((pb.ALG_GLYNN, pb.ALG_GLYNN_PLAIN), (pb.ALG_RYSER, pb.ALG_RYSER_PLAIN)):
+            x, y = pb.plan(n, a), pb.plan(n, p)
+            assert (x.chunk_bits, x.leaf_bits, x.block_bits, x.unit_bits) == (y.chunk_bits, y.leaf_bits, y.block_bits, y.unit_bits)
 
 
 def test_plan_large_n_shards_eight_ways():

@@ -75,3 +75,42 @@ def test_unit_range_tiles():
                 assert b == c
             if units % world == 0:
                 assert len({b - a for a, b in spans}) == 1
+
+
+def _oracle_batched(As):
+    import oracle
+    return torch.tensor([oracle.glynn(a).value for a in As.numpy()], dtype=torch.complex128)
+
+
+def _batched_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_1606_05836_b200.dist import batched_dist
+    As = torch.from_numpy(synth.haar_batch(7, 64, 8, 5, 6))      # 7 items: ragged over 2 ranks
+    out = batched_dist(As, fn=_oracle_batched)
+    out_q.put((rank, out.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_gloo_batched_sharding_one_all_gather():
+    """batch items sharded over ranks, one all_gather, ragged split (7 over 2)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batched_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import oracle
+    import synth
+    As = synth.haar_batch(7, 64, 8, 5, 6)
+    want = np.array([oracle.glynn(a).value for a in As])
+    for _, out in res:
+        assert out.shape == (7,)
+        assert np.array_equal(out, want)

@@ -1,0 +1,116 @@
+"""Checkpoint / resume and dynamic segment claims of paper_1606_05836_b200/runner.py on CPU
+(gloo, world_size 2).  The per-unit partial sums come from the oracle in place
+of the CUDA sweep and the canonical pairwise tree is done in Python with the oracle's dd
+addition (the GPU versions are exercised by tests/test_gpu_runner.py); what is tested here is
+the host logic: ledgers, resume, claims, the exact gather -- the result of an interrupted and
+resumed 2-rank run must equal the uninterrupted single-process run bit for bit."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+N = 20
+SEG = 16
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def oracle_sweep(A, alg, lo, hi):
+    import oracle
+    import paper_1606_05836_b200 as pb
+    a = A.numpy()
+    P = pb.plan(a.shape[0], alg)
+    out = [oracle.glynn_partial(a, u * P.unit_terms, (u + 1) * P.unit_terms, threads=1)[0].as4() for u in range(lo, hi)]
+    return torch.from_numpy(np.stack(out))
+
+
+def tree_combine(parts, n, alg, scale=True):
+    """Canonical tree (left + right, zero padding to a power of two) with the oracle's dd add."""
+    import oracle
+    v = [oracle.DD.from4(r) for r in parts.numpy()]
+    size = 1
+    while size < len(v):
+        size *= 2
+    v += [oracle.DD(0.0, 0.0, 0.0, 0.0)] * (size - len(v))
+    while len(v) > 1:
+        v = [v[i] + v[i + 1] for i in range(0, len(v), 2)]
+    root = v[0]
+    val = root.scaled(-(n - 1)).to_complex() if scale else None
+    return torch.tensor(val, dtype=torch.complex128), torch.from_numpy(root.as4())
+
+
+def _worker(rank, world, port, prefix, max_segments, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_1606_05836_b200.runner import run_checkpointed
+    A = torch.from_numpy(synth.gaussian(N, 321))
+    val, complete = run_checkpointed(A, "glynn", prefix, segment_units=SEG, max_segments=max_segments,
+                                     sweep=oracle_sweep, combine=tree_combine)
+    out_q.put((rank, None if val is None else complex(val.item()), complete))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _launch(world, prefix, max_segments):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, prefix, max_segments, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def test_interrupted_resumed_run_is_bit_identical(tmp_path):
+    import synth
+    import oracle
+    from paper_1606_05836_b200.runner import Ledger, run_checkpointed
+    prefix = str(tmp_path / "job")
+    # phase 1: both ranks stop after one segment each (a simulated failure)
+    res = _launch(2, prefix, 1)
+    assert all(v is None and not c for _, v, c in res)
+    ledgers = [Ledger.load(prefix + f".rank{r}.npz") for r in range(2)]
+    assert sorted(int(k) for L in ledgers for k in L.seg_done) == sorted(set(int(k) for L in ledgers for k in L.seg_done))
+    assert sum(len(L.seg_done) for L in ledgers) == 2
+    # phase 2: resume; the remaining segments are claimed dynamically
+    res = _launch(2, prefix, None)
+    vals = [v for _, v, c in res]
+    assert all(c for _, _, c in res) and vals[0] == vals[1]
+    ledgers = [Ledger.load(prefix + f".rank{r}.npz") for r in range(2)]
+    done = sorted(int(k) for L in ledgers for k in L.seg_done)
+    assert done == list(range(128 // SEG))                      # every segment exactly once
+    # reference: one process, no checkpoint
+    A = torch.from_numpy(synth.gaussian(N, 321))
+    ref, ok = run_checkpointed(A, "glynn", None, segment_units=SEG, sweep=oracle_sweep, combine=tree_combine)
+    assert ok and complex(ref.item()) == vals[0]
+    want = oracle.glynn(A.numpy()).value
+    assert abs(vals[0] - want) <= 1e-24 * abs(want) + 1e-300
+
+
+def test_ledger_of_another_job_is_rejected(tmp_path):
+    import synth
+    from paper_1606_05836_b200.runner import run_checkpointed
+    prefix = str(tmp_path / "job")
+    A = torch.from_numpy(synth.gaussian(N, 321))
+    v, ok = run_checkpointed(A, "glynn", prefix, segment_units=SEG, max_segments=1, sweep=oracle_sweep,
+                             combine=tree_combine)
+    assert v is None and not ok
+    B = torch.from_numpy(synth.gaussian(N, 322))
+    with pytest.raises(ValueError):
+        run_checkpointed(B, "glynn", prefix, segment_units=SEG, sweep=oracle_sweep, combine=tree_combine)
