@@ -120,6 +120,15 @@ int perm_ryser_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream);
 int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_t unit_hi,
                      perm_dd_c128* unit_partials, void* stream);
 
+/* Experiments / profiling: the same sweep kernel on a NON-canonical plan of (n, alg) with the
+ * given chunk_bits (5..12), leaf_bits (>= 0) and block_bits (0..7; dd: 0..6); units =
+ * 2^(log2_terms - chunk_bits - leaf_bits - block_bits) (<= 2^40).  Lets a profiler run the
+ * n = 50 kernel on short units (the canonical n = 50 unit is 2^32 terms, ~10 s per block).
+ * Partials follow that plan's unit numbering; combining all of them gives Perm(A) up to
+ * rounding (not bit-identical to the canonical plan). */
+int perm_sweep_units_custom(const perm_c128* A, int n, int alg, int chunk_bits, int leaf_bits, int block_bits,
+                            int64_t unit_lo, int64_t unit_hi, perm_dd_c128* unit_partials, void* stream);
+
 /* Unscaled partial over Gray indices [lo, hi) (any lo <= hi <= #terms; ragged ends are
  * walked by the library).  partial: device, 1 element.  If [lo, hi) is an aligned
  * power-of-two block of units, the value equals that node of the canonical tree. */

@@ -28,7 +28,7 @@ from ._lib import (ALG_GLYNN, ALG_GLYNN_DD, ALG_GLYNN_PLAIN, ALG_RYSER, ALG_RYSE
 
 __all__ = ["glynn", "ryser", "glynn_batched", "glynn_range", "ryser_range", "sweep_units", "combine",
            "glynn_host", "ryser_host", "glynn_batched_host", "plan", "max_n", "Plan", "PermError",
-           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "ALG_GLYNN_PLAIN", "ALG_RYSER_PLAIN", "glynn_dd", "ryser_dd", "range_partial", "perm_alg",
+           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "ALG_GLYNN_PLAIN", "ALG_RYSER_PLAIN", "glynn_dd", "ryser_dd", "range_partial", "perm_alg", "sweep_units_custom",
            "dd_to_complex"]
 
 
@@ -171,6 +171,21 @@ def sweep_units(A: torch.Tensor, alg, unit_lo: int, unit_hi: int) -> torch.Tenso
         _lib.check(_lib.lib().perm_sweep_units(A.data_ptr(), n, a, int(unit_lo), int(unit_hi),
                                                out.data_ptr() if count > 0 else None, _stream(A.device)),
                    "perm_sweep_units")
+    return out
+
+
+def sweep_units_custom(A: torch.Tensor, alg, chunk_bits: int, leaf_bits: int, block_bits: int,
+                       unit_lo: int, unit_hi: int) -> torch.Tensor:
+    """The sweep kernel on a non-canonical plan (profiling / experiments): (count, 4) float64."""
+    n = _square(A)
+    A = A.contiguous()
+    count = int(unit_hi) - int(unit_lo)
+    out = torch.empty((max(count, 0), 4), dtype=torch.float64, device=A.device)
+    with torch.cuda.device(A.device):
+        _lib.check(_lib.lib().perm_sweep_units_custom(A.data_ptr(), n, _alg(alg), int(chunk_bits), int(leaf_bits),
+                                                      int(block_bits), int(unit_lo), int(unit_hi),
+                                                      out.data_ptr() if count > 0 else None, _stream(A.device)),
+                   "perm_sweep_units_custom")
     return out
 
 

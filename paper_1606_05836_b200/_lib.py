@@ -18,7 +18,7 @@ ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD, ALG_GLYNN_PLAIN, ALG_RYSER_PLA
 EXPORTS = (
     "perm_max_n", "perm_strerror", "perm_plan", "perm_glynn", "perm_ryser", "perm_sweep_units",
     "perm_glynn_range", "perm_ryser_range", "perm_combine", "perm_glynn_batched", "perm_glynn_host",
-    "perm_ryser_host", "perm_glynn_batched_host", "perm_glynn_dd", "perm_ryser_dd", "perm_range",
+    "perm_ryser_host", "perm_glynn_batched_host", "perm_glynn_dd", "perm_ryser_dd", "perm_range", "perm_sweep_units_custom",
 )
 
 
@@ -79,6 +79,7 @@ def lib() -> ctypes.CDLL:
         L.perm_glynn_dd.argtypes = [vp, i32, vp, vp]
         L.perm_ryser_dd.argtypes = [vp, i32, vp, vp]
         L.perm_range.argtypes = [vp, i32, i32, u64, u64, vp, vp]
+        L.perm_sweep_units_custom.argtypes = [vp, i32, i32, i32, i32, i32, i64, i64, vp, vp]
         L.perm_glynn_host.argtypes = [vp, i32, vp]
         L.perm_ryser_host.argtypes = [vp, i32, vp]
         L.perm_glynn_batched_host.argtypes = [vp, i32, i64, vp]

@@ -324,6 +324,31 @@ int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_
   return rc;
 }
 
+int perm_sweep_units_custom(const perm_c128* A, int n, int alg, int chunk_bits, int leaf_bits, int block_bits,
+                            int64_t unit_lo, int64_t unit_hi, perm_dd_c128* unit_partials, void* stream) {
+  if (!A || !unit_partials || !valid_n_alg(n, alg)) return PERM_EINVAL;
+  perm_plan_t P;
+  make_plan(n, alg, &P);
+  const int wmax = is_dd(alg) ? 6 : 7;
+  if (chunk_bits < 5 || chunk_bits > kCMax || leaf_bits < 0 || block_bits < 0 || block_bits > wmax ||
+      chunk_bits + leaf_bits + block_bits > P.log2_terms || P.log2_terms - chunk_bits - leaf_bits - block_bits > 40)
+    return PERM_EINVAL;
+  P.chunk_bits = chunk_bits; P.leaf_bits = leaf_bits; P.block_bits = block_bits;
+  P.unit_bits = P.log2_terms - chunk_bits - leaf_bits - block_bits;
+  P.units = 1LL << P.unit_bits;
+  P.unit_terms = 1ULL << (P.log2_terms - P.unit_bits);
+  if (unit_lo < 0 || unit_lo > unit_hi || unit_hi > P.units || unit_hi - unit_lo > (1LL << 31) - 1) return PERM_EINVAL;
+  if (unit_lo == unit_hi) return PERM_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, kStagingBytes, st), "cudaMallocAsync");
+  const uint64_t lo = (uint64_t)unit_lo * P.unit_terms, hi = (uint64_t)unit_hi * P.unit_terms;
+  int rc = run_sweep(A, P, unit_lo, unit_hi, lo, hi, reinterpret_cast<Dd2*>(unit_partials), static_cast<double2*>(ws), st);
+  cudaError_t e = cudaFreeAsync(ws, st);
+  if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return rc;
+}
+
 int perm_glynn_range(const perm_c128* A, int n, uint64_t lo, uint64_t hi, perm_dd_c128* partial, void* stream) {
   return range_perm(A, n, PERM_ALG_GLYNN, lo, hi, partial, static_cast<cudaStream_t>(stream));
 }

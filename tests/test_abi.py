@@ -88,3 +88,16 @@ def test_plan_large_n_shards_eight_ways():
     for n in (32, 40, 50):
         P = pb.plan(n)
         assert P.units % 8 == 0 and P.units >= 4096
+
+
+def test_custom_plan_arguments_validated_without_cuda():
+    L = _lib.lib()
+    buf = ctypes.create_string_buffer(64)
+    f = L.perm_sweep_units_custom
+    assert f(buf, 20, 0, 4, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL      # chunk_bits < 5
+    assert f(buf, 20, 0, 13, 0, 0, 0, 1, buf, None) == _lib.PERM_EINVAL     # chunk_bits > 12
+    assert f(buf, 20, 0, 10, 0, 8, 0, 1, buf, None) == _lib.PERM_EINVAL     # block_bits > 7
+    assert f(buf, 20, 2, 10, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL     # dd: block_bits > 6
+    assert f(buf, 20, 0, 10, 5, 7, 0, 1, buf, None) == _lib.PERM_EINVAL     # c + lam + wb > 19
+    assert f(buf, 20, 0, 10, 0, 7, 0, 5, buf, None) == _lib.PERM_EINVAL     # unit_hi > units (4)
+    assert f(buf, 20, 0, 10, 0, 7, 0, 0, buf, None) == _lib.PERM_OK         # empty

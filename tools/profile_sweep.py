@@ -3,6 +3,7 @@ units, so `ncu --set full` replays stay short.
 
     python tools/profile_sweep.py [--workload M4] [--fraction 64 | --units U] [--alg glynn] [--reps 2]
     python tools/profile_sweep.py --workload M2 --batched [--reps 2]
+    python tools/profile_sweep.py --workload M5 --custom 11,4,7 --units 296   # short n = 50 units
 
 --alg: glynn | ryser | glynn_dd | ryser_dd.  --batched times perm_glynn_batched on M2.
 """
@@ -25,6 +26,7 @@ ap.add_argument("--units", type=int, default=0, help="sweep exactly this many un
 ap.add_argument("--alg", default="glynn")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--batched", action="store_true")
+ap.add_argument("--custom", default="", help="c,leaf_bits,block_bits: non-canonical plan (perm_sweep_units_custom)")
 a = ap.parse_args()
 A = torch.from_numpy(synth.workload(a.workload)).cuda()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,10 +45,17 @@ if a.batched:
 n = A.shape[0]
 alg = pb._alg(a.alg)
 P = pb.plan(n, alg)
+if a.custom:
+    c, lam, wb = (int(x) for x in a.custom.split(","))
+    ub = P.log2_terms - c - lam - wb
+    P = pb.Plan(n, alg, P.log2_terms, c, lam, wb, ub, 1 << (P.log2_terms - ub), 1 << ub)
 units = a.units or max(1, P.units // a.fraction)
 for r in range(a.reps):
     e0.record()
-    parts = pb.sweep_units(A, alg, 0, units)
+    if a.custom:
+        parts = pb.sweep_units_custom(A, alg, P.chunk_bits, P.leaf_bits, P.block_bits, 0, units)
+    else:
+        parts = pb.sweep_units(A, alg, 0, units)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
