@@ -98,7 +98,16 @@ void make_plan(int n, int alg, perm_plan_t* p) {
     const int ub_min = rem - 5 < 7 ? rem - 5 : 7;
     c = rem - ub_min < ct ? rem - ub_min : ct;
     if (c < 5) c = 5;
-    ubits = rem - c < 17 ? rem - c : 17;
+    // Units: 2^17 up to 2^39 terms; beyond, 2^(m-29) (capped at 2^22) so a unit stays ~2^29
+    // terms (~3 s per wave at n = 50).  Long units make every wave one lock-step phase: the
+    // two co-resident blocks of an SM build their chunks at the same moments, and a single
+    // 2^32-term wave measured 0.83 of the FP64 issue rate against 0.87 for 8 short waves
+    // (tools/profile_sweep.py --custom, 2026-10-20).  Short units also make checkpoint
+    // segments and multi-GPU shares finer.
+    int ucap = m - 29;
+    if (ucap < 17) ucap = 17;
+    if (ucap > 22) ucap = 22;
+    ubits = rem - c < ucap ? rem - c : ucap;
     lam = rem - c - ubits;
   }
   p->n = n; p->alg = alg;

@@ -102,14 +102,19 @@ __device__ __forceinline__ Dd2 dd2_add(const Dd2& a, const Dd2& b) {
   return r;
 }
 
-// Number of independent product chains for n.  4 gives the most ILP, but near the 255-register
-// cap (4n registers of row sums) ptxas's allocation of the half-walk loop is erratic: per n, the
-// chain count below is the one whose loop has no local-memory spills and the fewest register
-// moves in the SASS (tools/sass_loop_stats.py, 2026-10-19: n = 50 with 4 chains spilled 28
-// accesses and moved 205 registers per 4 terms; with 3 chains: 0 spills, 32 moves).  Beyond
-// n = 53 every count spills; 2 is the least bad.
+// Register budget near the 255-register cap (4n registers of row sums).  ptxas's allocation of
+// the half-walk loop is erratic there, so two shape parameters are chosen per n from the SASS
+// of the loop (tools/sass_loop_stats.py over all variants, 2026-10-20; register moves /
+// local-memory spill instructions per 4 terms):
+//   acc_in_smem: the chunk's Sum2 accumulator lives in a per-thread shared-memory slot
+//     (touched once per 16 terms) instead of 8 registers;
+//   product_chains: independent chains of the n-way complex product.
+//   n <= 50: smem accumulator + 4 chains: 10 / 0 (register accumulator: n = 50 206 / 28 with
+//     4 chains, 32 / 2 with 3);  n = 51: smem + 3: 10 / 0;  n = 52: registers + 3: 68 / 28;
+//   n = 53: smem + 3: 192 / 20;  n >= 54: registers + 2: 70 / 16 (n = 54) .. 184 / 40 (56).
+__host__ __device__ constexpr bool acc_in_smem(int N) { return N <= 51 || N == 53; }
 __host__ __device__ constexpr int product_chains(int N) {
-  return N < 4 ? N : (N == 49 || N >= 54) ? 2 : (N == 50 || N == 53) ? 3 : 4;
+  return N < 4 ? N : N <= 50 ? 4 : N <= 53 ? 3 : 2;
 }
 
 // Product of the n row sums: NC independent chains (i mod NC) then a pairwise tree.
@@ -140,6 +145,7 @@ __device__ __forceinline__ double2 row_product(const double2 (&s)[N]) {
 static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 
 struct ConstColumns {
+  static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
   int base;
   __device__ __forceinline__ double2 get(int row, int i) const { return c_cols[base + row * kNMax + i]; }
 };
@@ -148,6 +154,9 @@ struct ConstColumns {
 // tab[(2b+d)*N + i] = signed step vector of Gray bit b, direction d (zero rows for b >= c).
 template <int N>
 struct SmemColumns {
+  // The batched kernel reads its columns from shared memory; with shared-memory accumulators
+  // too (and their layout) M2 measured 28 % slower (1.11 vs 0.865 ms): registers there.
+  static constexpr bool kSmemAccOk = false;
   const double2* tab;
   __device__ __forceinline__ double2 get(int row, int i) const { return tab[row * N + i]; }
 };
@@ -168,10 +177,15 @@ __device__ __forceinline__ Dd2 part_add(const Dd2& a, const Dd2& b) {
 // PLAIN = false: compensated accumulation (Sum2 cascade + dd partials, the default);
 // PLAIN = true: every accumulation in plain FP64 (the precision lab's "plain" mode, §8(f)2:
 // same terms, same order, only the compensation removed).
-template <int N, int ALG, bool PLAIN = false>
+template <int N, int ALG, bool PLAIN = false, bool SMEM_ACC = acc_in_smem(N)>
 struct Walker {
   double2 s[N];                  // row sums (registers)
-  double arh, arl, aih, ail;     // cascaded (Sum2) double-double accumulators (PLAIN: arh, aih only)
+  // Cascaded (Sum2) double-double accumulator of the chunk (PLAIN: hi halves only): in
+  // registers, or (acc_in_smem(N)) in this thread's shared-memory slot, which the kernels place
+  // right after their N*N matrix copy and blockDim reduction entries.
+  static constexpr bool kSmemAcc = SMEM_ACC;
+  double arh, arl, aih, ail;
+  Dd2* accs;
 
   // Column sources hold STEP VECTORS u = kScale * column (Glynn 2a: exact doubling; Ryser a).
   // Direction bit d of a flip: Glynn d=1 -> delta back to +1 -> +u, d=0 -> delta to -1 -> -u;
@@ -182,9 +196,32 @@ struct Walker {
   // term sign base: Glynn (-1)^g ; Ryser (-1)^(N+g)
   static constexpr bool kNegBase = (ALG == kRyser) && (N & 1);
 
-  __device__ __forceinline__ void zero_acc() { arh = arl = aih = ail = 0.0; }
+  __device__ __forceinline__ void zero_acc() {
+    if (kSmemAcc) {
+      extern __shared__ double2 smem_acc[];
+      accs = reinterpret_cast<Dd2*>(smem_acc + N * N) + blockDim.x + threadIdx.x;
+      *accs = Dd2{0.0, 0.0, 0.0, 0.0};
+    } else {
+      arh = arl = aih = ail = 0.0;
+    }
+  }
 
   __device__ __forceinline__ void acc_add(double re, double im) {
+    if (kSmemAcc) {
+      Dd2 a = *accs;
+      if (PLAIN) {
+        a.re_hi = __dadd_rn(a.re_hi, re);
+        a.im_hi = __dadd_rn(a.im_hi, im);
+      } else {
+        double s_, e_;
+        two_sum(a.re_hi, re, s_, e_);
+        a.re_hi = s_; a.re_lo = __dadd_rn(a.re_lo, e_);
+        two_sum(a.im_hi, im, s_, e_);
+        a.im_hi = s_; a.im_lo = __dadd_rn(a.im_lo, e_);
+      }
+      *accs = a;
+      return;
+    }
     if (PLAIN) {
       arh = __dadd_rn(arh, re);
       aih = __dadd_rn(aih, im);
@@ -325,6 +362,14 @@ struct Walker {
   }
 
   __device__ __forceinline__ Dd2 result() const {
+    if (kSmemAcc) {
+      const Dd2 a = *accs;
+      if (PLAIN) return Dd2{a.re_hi, 0.0, a.im_hi, 0.0};
+      Dd2 r;
+      fast_two_sum(a.re_hi, a.re_lo, r.re_hi, r.re_lo);
+      fast_two_sum(a.im_hi, a.im_lo, r.im_hi, r.im_lo);
+      return r;
+    }
     if (PLAIN) return Dd2{arh, 0.0, aih, 0.0};
     Dd2 r;
     fast_two_sum(arh, arl, r.re_hi, r.re_lo);
@@ -337,18 +382,18 @@ struct Walker {
 // in a separate ptxas allocation unit is what lets ptxas hold the half-walk loop counter in
 // a uniform register and feed the column operands from LDCU; inlined into the leaf loop
 // (a loop nest with the build's loop) it fell back to per-thread LDC and spilled.
-template <int N, int ALG, bool PLAIN, class Cols>
+template <int N, int ALG, bool PLAIN, bool SA, class Cols>
 __device__ __noinline__ Dd2 chunk_fast(const Cols cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
-  Walker<N, ALG, PLAIN> w;
+  Walker<N, ALG, PLAIN, SA> w;
   w.zero_acc();
   w.fast_chunk(cols, at, q, c, zero);
   return w.result();
 }
 
 // Ragged piece [ga, gb) of one chunk (range ends, tiny n).
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, bool PLAIN, bool SA>
 __device__ __noinline__ Dd2 chunk_generic(const double2* __restrict__ at, uint64_t ga, uint64_t gb) {
-  Walker<N, ALG, PLAIN> w;
+  Walker<N, ALG, PLAIN, SA> w;
   w.zero_acc();
   w.generic_walk(at, ga, gb);
   return w.result();
@@ -373,6 +418,9 @@ __device__ __forceinline__ void leaf_chunk_window(uint64_t leaf_id, int c, int l
 template <int N, int ALG, bool kFast, bool PLAIN, class Cols>
 __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
                                          int c, int lam, uint64_t lo, uint64_t hi, int zero) {
+  // shared-memory chunk accumulator only in the sweep kernel (ConstColumns; its smem layout
+  // puts the slots after the matrix copy and the reduction entries)
+  constexpr bool SA = Cols::kSmemAccOk && acc_in_smem(N);
   Dd2 acc{0.0, 0.0, 0.0, 0.0};
   // Fast path: all 2^lam chunks (this exact loop shape keeps ptxas's uniform-register column
   // path, tests/test_build_sass.py).  Ragged path: only chunks [k0, k1) meeting [lo, hi).
@@ -381,12 +429,12 @@ __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __rest
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t q = (leaf_id << lam) + k;
     if (kFast) {
-      acc = part_add<PLAIN>(acc, chunk_fast<N, ALG, PLAIN>(cols, at, q, c, zero));
+      acc = part_add<PLAIN>(acc, chunk_fast<N, ALG, PLAIN, SA>(cols, at, q, c, zero));
     } else {
       const uint64_t g0 = q << c, g1 = g0 + (1ull << c);
       const uint64_t ga = g0 > lo ? g0 : lo;
       const uint64_t gb = g1 < hi ? g1 : hi;
-      if (ga < gb) acc = part_add<PLAIN>(acc, chunk_generic<N, ALG, PLAIN>(at, ga, gb));
+      if (ga < gb) acc = part_add<PLAIN>(acc, chunk_generic<N, ALG, PLAIN, SA>(at, ga, gb));
     }
   }
   return acc;
@@ -424,6 +472,7 @@ __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
 template <int N, int ALG, bool PLAIN>
 __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
+  // [N*N: at][blockDim Dd2: tree][blockDim Dd2: chunk accumulators (Walker)]
   double2* at = smem;
   Dd2* red = reinterpret_cast<Dd2*>(smem + N * N);
   stage_transposed<N>(args.A, at, Walker<N, ALG>::kScale);
@@ -455,6 +504,7 @@ __host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? 4
 template <int N>
 __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kernel(const BatchedArgs args) {
   extern __shared__ double2 smem[];
+  // [N*N: at][kTabRows*N: tab][blockDim Dd2: tree]  (register chunk accumulators)
   double2* at = smem;
   double2* tab = smem + N * N;
   Dd2* red = reinterpret_cast<Dd2*>(smem + N * N + kTabRows * N);
@@ -526,7 +576,7 @@ cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cu
     if (e != cudaSuccess) return e;
   }
   const int threads = 1 << a.block_bits;
-  const size_t smem = sizeof(double2) * N * N + sizeof(Dd2) * threads;
+  const size_t smem = sizeof(double2) * N * N + 2 * sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -73,7 +73,7 @@ def test_plan_is_a_partition(alg):
         assert 0 <= P.block_bits <= (6 if alg in (pb.ALG_GLYNN_DD, pb.ALG_RYSER_DD) else 7) and 0 <= P.chunk_bits <= 12
         if m >= 5:
             assert P.chunk_bits >= 5                       # fast path usable
-        assert P.units <= 1 << 17
+        assert P.units <= 1 << 22 and (P.units <= 1 << 17 or P.unit_terms >= 1 << 29)
 
 
 def test_plain_mode_plans_equal_fp64_plans():

@@ -8,7 +8,7 @@ quotes for the other configs.
   M2  4096 x 16x16 batched Glynn: permanents/s, terms/s, FP64 fraction
   M3  n=32: Glynn / Ryser seconds, terms/s
   M4  n=40: Glynn + Ryser full permanents; Glynn-Ryser discrepancy (class X)
-  M5  n=50: sweep of the first 296 canonical units (one full wave: 2 resident blocks x 148
+  M5  n=50: sweep of the first 2368 canonical units (8 waves of 2 resident blocks x 148
       SMs; Glynn and Ryser), per-GPU terms/s and the extrapolated 1- and 8-GPU seconds
   DD  the double-double mode on M1 (n=20) and M3 (n=32): ms and terms/s
 """
@@ -26,6 +26,7 @@ import torch  # noqa: E402
 
 import synth  # noqa: E402
 import paper_1606_05836_b200 as pb  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 PEAK_INSTR = 148 * 64 * 1.965e9          # FP64 pipe instructions/s
 
@@ -51,7 +52,7 @@ def rates(n, terms, ms, per_term_instr=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "perf_configs.json"))
-    ap.add_argument("--m5-units", type=int, default=296, help="units per M5 sample (2 resident blocks x 148 SMs)")
+    ap.add_argument("--m5-units", type=int, default=2368, help="units per M5 sample (8 waves of 2 resident blocks x 148 SMs)")
     ap.add_argument("--skip", default="")
     a = ap.parse_args()
     skip = set(a.skip.split(",")) if a.skip else set()
@@ -103,12 +104,18 @@ def main():
             P = pb.plan(50, alg)
             units = a.m5_units
             pb.range_partial(A, alg, 0, 4096)          # loads the n = 50 kernel
+            clk = ClockSampler(0)
+            clk.start()
             ms, _ = ev_time(lambda: pb.sweep_units(A, alg, 0, units), 1)
+            clocks = clk.stop()
             terms = units * P.unit_terms
             x = rates(50, terms, ms)
             x["full_seconds_1gpu_extrapolated"] = P.terms / x["terms_per_s"]
             x["full_seconds_8gpu_extrapolated"] = P.terms / x["terms_per_s"] / 8
             x["units_swept"] = units
+            x["clocks"] = clocks
+            if clocks.get("sm_mhz"):
+                x["fp64_instr_frac_at_measured_clock"] = x["fp64_instr_frac"] * 1965.0 / clocks["sm_mhz"]
             r[name] = x
         res["M5"] = r
 
