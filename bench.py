@@ -33,6 +33,9 @@ SM_COUNT = 148                 # B200 (B200_PROFILING.md)
 SM_MAX_MHZ = 1965.0            # clocks.max.sm (B200_PROFILING.md / MEASURED_PEAKS.json)
 FP64_FMA_PER_SM_CLK = 64       # FP64 lanes per SM (measured 34 TFLOP/s DFMA)
 FP64_PEAK_TFLOPS = SM_COUNT * FP64_FMA_PER_SM_CLK * 2 * SM_MAX_MHZ * 1e6 / 1e12   # 37.2
+# Sustained DFMA rate measured on this pool's B200 (tools/microbench/fp64_probe.cu, 8 independent
+# DFMA chains per thread, 32 warps/SM, 0.9 s, 1965 MHz throughout): profiles/r01_fp64_probe.log
+FP64_MEASURED_TFLOPS = 33.84
 
 
 def _env_int(name, default):
@@ -274,7 +277,12 @@ def run_ours(args, rank, world, local_rank):
                      "traffic_note": "dram bytes of the ncu --set full launch (2048 of the plan's units; profiles/)",
                      "kernel": "sweep_kernel (perm_sweep_units)", "flop_per_term": flop_per_term,
                      "fp64_instr_frac": instr_frac,
-                     "peak_note": "derived FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §Roofline)"},
+                     "peak_note": "derived FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §Roofline)",
+                     "measured_peak": FP64_MEASURED_TFLOPS,
+                     "frac_of_measured": achieved / FP64_MEASURED_TFLOPS,
+                     "fp64_issue_frac_of_measured": instr_frac * FP64_PEAK_TFLOPS / FP64_MEASURED_TFLOPS,
+                     "measured_peak_note": "sustained DFMA microbenchmark, profiles/r01_fp64_probe.log; "
+                                           "algorithmic ceiling (8n-4)/(2(6n-2)) = 0.664 of any DFMA peak"},
         "e2e": {"value": terms / (e2e_ms_step * 1e-3), "unit": "terms/s", "h2d_bytes_per_step": 16 * n * n,
                 "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms_step},
         "gpu_launches": 4 * args.steps,
