@@ -27,6 +27,7 @@ from __future__ import annotations
 import glob
 import hashlib
 import os
+import time
 from dataclasses import dataclass
 from typing import Callable, Optional
 
@@ -82,13 +83,16 @@ def _load_all(prefix: str, n: int, alg: int, units: int, seg_units: int, sha: st
 
 
 def run_checkpointed(A: torch.Tensor, alg="glynn", prefix: Optional[str] = None, segment_units: int = 0,
-                     group=None, store=None, max_segments: Optional[int] = None,
-                     sweep: Optional[Callable] = None, combine: Optional[Callable] = None):
+                     group=None, store=None, max_segments: Optional[int] = None, deadline: Optional[float] = None,
+                     sweep: Optional[Callable] = None, combine: Optional[Callable] = None,
+                     on_segment: Optional[Callable] = None):
     """Perm(A) by `alg` as claimed, checkpointed segments of the canonical plan's units.
 
     Returns (value, complete): value is the 0-d complex128 permanent (None if this call stopped
     early because `max_segments` segments were computed by this rank -- a simulated failure
-    for tests), identical on every rank and bit-identical to the one-shot computation.
+    for tests -- or because time.monotonic() passed `deadline`; the ledgers keep the work),
+    identical on every rank and bit-identical to the one-shot computation.
+    `on_segment(k, lo, hi)` is called after each segment this rank computes (progress logs).
     `prefix`: ledger path prefix (None: no checkpointing).  `segment_units`: units per segment
     (0: units / 64).  `store`: torch.distributed Store for the claim counter (default: the
     default group's store).  `sweep` / `combine` default to the CUDA kernels."""
@@ -129,7 +133,8 @@ def run_checkpointed(A: torch.Tensor, alg="glynn", prefix: Optional[str] = None,
     stopped = False
     next_local = 0
     while True:
-        if max_segments is not None and computed >= max_segments:
+        if (max_segments is not None and computed >= max_segments) or \
+                (deadline is not None and time.monotonic() > deadline):
             stopped = True
             break
         if world > 1:
@@ -150,6 +155,8 @@ def run_checkpointed(A: torch.Tensor, alg="glynn", prefix: Optional[str] = None,
         if prefix:
             Ledger(n, a, P.units, seg_units, sha, np.asarray(mine_k, np.int64),
                    np.concatenate(mine_parts, axis=0)).save(prefix + f".rank{rank}.npz")
+        if on_segment is not None:
+            on_segment(k, lo, hi)
 
     stop_any = torch.tensor([1 if stopped else 0], dtype=torch.int64)
     table = np.zeros((P.units, 4), np.float64)
