@@ -40,6 +40,7 @@ DeviceSlots g_slots[64];
 
 std::once_flag g_tables_once;
 SweepLauncher g_sweep[6][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN
+SweepLauncher g_small[6][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -64,6 +65,7 @@ void init_tables() {
     register_dd_glynn_b(g_sweep[PERM_ALG_GLYNN_DD]);
     register_dd_ryser_a(g_sweep[PERM_ALG_RYSER_DD]);
     register_dd_ryser_b(g_sweep[PERM_ALG_RYSER_DD]);
+    register_small(g_small);
     register_batched_a(g_batched);
     register_batched_b(g_batched);
   });
@@ -195,6 +197,12 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   a.unit_lo = u_lo;
   a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
   a.zero = 0;
+  if (!is_dd(P.alg) && P.log2_terms <= kSmallLog2 && g_small[P.alg][P.n]) {
+    // small n: columns from shared memory, no staging / constant slot / fencing
+    a.slot = 0; a.col_base = 0;
+    CUDA_TRY(g_small[P.alg][P.n](a, u_hi - u_lo, staging, st), "small sweep launch");
+    return PERM_OK;
+  }
   if (is_dd(P.alg)) {            // the dd sweep reads its columns from A: no constant slot
     a.slot = 0; a.col_base = 0;
     CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "dd sweep launch");

@@ -491,6 +491,56 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) 
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
 }
 
+// Signed step-vector table of one matrix in shared memory, the layout of the constant one:
+// tab[(2b+d)*N + i] = step of Gray bit b (< c) flipped with direction d; zero rows beyond c.
+// at = the pre-scaled transposed matrix (Glynn 2a, Ryser a).
+template <int N, int ALG>
+__device__ __forceinline__ void build_tab(const double2* at, double2* tab, int c) {
+  constexpr int col0 = (ALG == kGlynn) ? 1 : 0;
+  for (int k = threadIdx.x; k < kTabRows * N; k += blockDim.x) {
+    const int row = k / N, i = k - row * N;
+    const int bb = row >> 1, d = row & 1;
+    double2 v = make_double2(0.0, 0.0);
+    if (bb < c && col0 + bb < N) {
+      v = at[(col0 + bb) * N + i];
+      // Glynn: d=1 -> +2a, d=0 -> -2a;  Ryser: d=1 -> -a, d=0 -> +a
+      const bool neg = (ALG == kGlynn) ? !d : d;
+      if (neg) { v.x = -v.x; v.y = -v.y; }
+    }
+    tab[k] = v;
+  }
+}
+
+// Small-n single permanents (2^m terms, m <= kSmallLog2): the same walk with the step vectors
+// read from a per-block shared-memory table (SmemColumns) instead of the constant bank, so a
+// call needs no column-staging kernel, no constant-memory copy and no slot fencing -- two
+// launches (this + combine) instead of four.  The terms and their order are the sweep
+// kernel's (same table values, same flips, same accumulation), i.e. bit-identical results.
+constexpr int kSmallLog2 = 21;
+
+template <int N, int ALG, bool PLAIN>
+__global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs args) {
+  extern __shared__ double2 smem[];
+  // [N*N: at][kTabRows*N: tab][blockDim Dd2: tree]  (register chunk accumulators)
+  double2* at = smem;
+  double2* tab = smem + N * N;
+  Dd2* red = reinterpret_cast<Dd2*>(smem + N * N + kTabRows * N);
+  stage_transposed<N>(args.A, at, Walker<N, ALG>::kScale);
+  __syncthreads();
+  build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
+  __syncthreads();
+  const SmemColumns<N> cols{tab};
+  const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
+  const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
+  const int ubits = args.block_bits + args.lam + args.c;
+  const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
+  Dd2 mine;
+  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  block_tree<PLAIN>(red, mine);
+  if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
+}
+
 // Batched Glynn: block b computes Perm(A_b) completely (boson sampling needs
 // many permanents of n x n submatrices).  Columns come from the block's shared-memory copy
 // (warp-uniform addresses: broadcast LDS).
@@ -585,6 +635,18 @@ cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cu
   return cudaGetLastError();
 }
 
+template <int N, int ALG, bool PLAIN>
+cudaError_t launch_sweep_small(const SweepArgs& a, int64_t units, double2*, cudaStream_t st) {
+  const int threads = 1 << a.block_bits;
+  const size_t smem = sizeof(double2) * (N * N + kTabRows * N) + sizeof(Dd2) * threads;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_small_kernel<N, ALG, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  sweep_small_kernel<N, ALG, PLAIN><<<(unsigned)units, threads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int N>
 cudaError_t launch_batched(const BatchedArgs& a, int grid, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
@@ -609,6 +671,10 @@ void fill_sweep(SweepLauncher* table, std::integer_sequence<int, Is...>) {
 template <int ALG, int LO, int... Is>
 void fill_sweep_plain(SweepLauncher* table, std::integer_sequence<int, Is...>) {
   ((table[LO + Is] = &launch_sweep<LO + Is, ALG, true>), ...);
+}
+template <int ALG, bool PLAIN, int LO, int... Is>
+void fill_sweep_small(SweepLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_sweep_small<LO + Is, ALG, PLAIN>), ...);
 }
 template <int LO, int... Is>
 void fill_batched(BatchedLauncher* table, std::integer_sequence<int, Is...>) {

@@ -45,3 +45,20 @@ def test_sweep_columns_are_uniform_operands(obj, n, alg):
     assert "DFMA" in k and "DMUL" in k
     for bad in ("HMMA", "UTCHMMA", "DMMA"):
         assert bad not in k
+
+
+@pytest.mark.parametrize("obj,n,alg", [("perm_inst_glynn_c.o", 40, 0), ("perm_inst_glynn_c.o", 48, 0),
+                                       ("perm_inst_glynn_c.o", 50, 0), ("perm_inst_ryser_c.o", 50, 1),
+                                       ("perm_inst_glynn_c.o", 51, 0)])
+def test_hot_loop_has_no_spills_up_to_n51(obj, n, alg):
+    """The register-budget choices (perm_kernels.cuh acc_in_smem / product_chains) keep the
+    half-walk loop free of local-memory traffic up to n = 51."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from sass_loop_stats import loop_stats
+    name, length, c = loop_stats(_sass(obj), f"sweep_kernelILi{n}ELi{alg}ELb0")
+    assert length > 0
+    spills = sum(v for k, v in c.items() if k.startswith(("STL", "LDL")))
+    assert spills == 0, (n, spills)
+    assert c["IMAD.MOV.U32"] + c["MOV"] <= 16, (n, c["IMAD.MOV.U32"] + c["MOV"])
+    assert c["DADD"] + c["DMUL"] + c["DFMA"] > 0
