@@ -29,7 +29,8 @@
  * Ownership and asynchrony: the CALLER owns every buffer.  Functions taking device
  * pointers enqueue work on `stream` (a cudaStream_t passed as void*; NULL = legacy
  * default stream) on the CURRENT device and return immediately; outputs are valid after
- * the stream is synchronised.  Temporary workspace is taken with cudaMallocAsync on
+ * the stream is synchronised.  Temporary workspace is taken stream-ordered (cudaMallocFromPoolAsync,
+ * a library-owned per-device pool that keeps up to 256 MiB cached) on
  * `stream` and released on it.  Concurrent calls on different streams / devices are
  * safe (the per-device constant-memory column slots are fenced with events).
  * Functions suffixed _host take HOST pointers and are synchronous.

@@ -38,6 +38,39 @@ struct DeviceSlots {
 };
 DeviceSlots g_slots[64];
 
+// Per-device stream-ordered memory pool for the library's temporary workspaces (staging table,
+// unit partials, host-entry copies).  The default pool's release threshold is 0: it returns
+// its memory at every synchronisation, so the next cudaMallocAsync maps fresh pages -- measured
+// 4.2 ms for a synchronous n = 20 call (tools/latency_probe.py).  This pool keeps up to
+// 256 MiB cached instead; concurrent streams allocate from it safely.
+struct DevicePool {
+  std::once_flag once;
+  cudaMemPool_t pool = nullptr;
+  cudaError_t err = cudaSuccess;
+};
+DevicePool g_pools[64];
+
+cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+  DevicePool& dp = g_pools[dev];
+  std::call_once(dp.once, [&] {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    dp.err = cudaMemPoolCreate(&dp.pool, &props);
+    if (dp.err == cudaSuccess) {
+      uint64_t thr = 256ull << 20;
+      dp.err = cudaMemPoolSetAttribute(dp.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  if (dp.err != cudaSuccess) return dp.err;
+  return cudaMallocFromPoolAsync(p, bytes, dp.pool, st);
+}
+
 std::once_flag g_tables_once;
 SweepLauncher g_sweep[6][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN
 SweepLauncher g_small[6][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
@@ -235,7 +268,7 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
   make_plan(n, alg, &P);
   void* ws = nullptr;
   const size_t bytes = kStagingBytes + sizeof(Dd2) * (size_t)P.units;
-  CUDA_TRY(cudaMallocAsync(&ws, bytes, st), "cudaMallocAsync");
+  CUDA_TRY(ws_alloc(&ws, bytes, st), "workspace alloc");
   double2* staging = static_cast<double2*>(ws);
   Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
   const uint64_t T = 1ULL << P.log2_terms;
@@ -261,7 +294,7 @@ int range_perm(const perm_c128* A, int n, int alg, uint64_t lo, uint64_t hi, per
   const int64_t u_hi = (int64_t)((hi + P.unit_terms - 1) / P.unit_terms);
   void* ws = nullptr;
   const size_t bytes = kStagingBytes + sizeof(Dd2) * (size_t)(u_hi - u_lo);
-  CUDA_TRY(cudaMallocAsync(&ws, bytes, st), "cudaMallocAsync");
+  CUDA_TRY(ws_alloc(&ws, bytes, st), "workspace alloc");
   double2* staging = static_cast<double2*>(ws);
   Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
   int rc = run_sweep(A, P, u_lo, u_hi, lo, hi, parts, staging, st);
@@ -333,7 +366,7 @@ int perm_sweep_units(const perm_c128* A, int n, int alg, int64_t unit_lo, int64_
   if (unit_lo == unit_hi) return PERM_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, kStagingBytes, st), "cudaMallocAsync");
+  CUDA_TRY(ws_alloc(&ws, kStagingBytes, st), "workspace alloc");
   const uint64_t lo = (uint64_t)unit_lo * P.unit_terms, hi = (uint64_t)unit_hi * P.unit_terms;
   int rc = run_sweep(A, P, unit_lo, unit_hi, lo, hi, reinterpret_cast<Dd2*>(unit_partials), static_cast<double2*>(ws), st);
   cudaError_t e = cudaFreeAsync(ws, st);
@@ -358,7 +391,7 @@ int perm_sweep_units_custom(const perm_c128* A, int n, int alg, int chunk_bits, 
   if (unit_lo == unit_hi) return PERM_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* ws = nullptr;
-  CUDA_TRY(cudaMallocAsync(&ws, kStagingBytes, st), "cudaMallocAsync");
+  CUDA_TRY(ws_alloc(&ws, kStagingBytes, st), "workspace alloc");
   const uint64_t lo = (uint64_t)unit_lo * P.unit_terms, hi = (uint64_t)unit_hi * P.unit_terms;
   int rc = run_sweep(A, P, unit_lo, unit_hi, lo, hi, reinterpret_cast<Dd2*>(unit_partials), static_cast<double2*>(ws), st);
   cudaError_t e = cudaFreeAsync(ws, st);
@@ -408,8 +441,8 @@ static int host_call(const perm_c128* A, int n, int64_t batch, perm_c128* out, i
   void* dO = nullptr;
   const size_t abytes = sizeof(perm_c128) * (size_t)n * n * batch, obytes = sizeof(perm_c128) * batch;
   int rc = PERM_OK;
-  cudaError_t e = cudaMallocAsync(&dA, abytes, st);
-  if (e == cudaSuccess) e = cudaMallocAsync(&dO, obytes, st);
+  cudaError_t e = ws_alloc(&dA, abytes, st);
+  if (e == cudaSuccess) e = ws_alloc(&dO, obytes, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dA, A, abytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) rc = cuda_fail(e, "host entry: alloc/copy in");
   if (rc == PERM_OK) {
