@@ -68,6 +68,11 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
     }
   });
   if (dp.err != cudaSuccess) return dp.err;
+  // under stream capture: a plain stream-ordered allocation becomes a graph memory node
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  if (cs != cudaStreamCaptureStatusNone) return cudaMallocAsync(p, bytes, st);
   return cudaMallocFromPoolAsync(p, bytes, dp.pool, st);
 }
 
@@ -235,6 +240,17 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
     a.slot = 0; a.col_base = 0;
     CUDA_TRY(g_small[P.alg][P.n](a, u_hi - u_lo, staging, st), "small sweep launch");
     return PERM_OK;
+  }
+  {
+    // The constant-slot path fences the slot with events recorded outside any graph; it is
+    // not capturable.  Fail loudly (small n, the dd mode and the batched kernel are).
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CUDA_TRY(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+    if (cs != cudaStreamCaptureStatusNone && !is_dd(P.alg)) {
+      g_last_error = "stream capture: the constant-memory column path (more than 2^21 terms) cannot be "
+                     "captured in a CUDA graph; capture small n, the dd mode or perm_glynn_batched";
+      return PERM_ECUDA;
+    }
   }
   if (is_dd(P.alg)) {            // the dd sweep reads its columns from A: no constant slot
     a.slot = 0; a.col_base = 0;

@@ -46,3 +46,21 @@ for fn in (pb.glynn, pb.ryser):
         lat.append(time.perf_counter() - s)
     lat.sort()
     print(f"{fn.__name__} n={a.n}: single-call synchronous latency median {lat[len(lat) // 2] * 1e6:.1f} us")
+
+# CUDA-graph replay of the same call (PermGraph): input copy + replay per permanent
+for alg in ("glynn", "ryser"):
+    g = pb.PermGraph(a.n, alg)
+    for _ in range(20):
+        g(A)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(a.calls):
+        g(A)
+    e1.record()
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    print(f"graph {alg} n={a.n}: host submit {(t1 - t0) / a.calls * 1e6:.1f} us/call, "
+          f"device span {e0.elapsed_time(e1) / a.calls * 1e3:.1f} us/call, wall {(t2 - t0) / a.calls * 1e6:.1f} us/call")
