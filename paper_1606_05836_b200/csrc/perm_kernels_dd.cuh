@@ -55,11 +55,11 @@ __device__ __forceinline__ dd dot2(dd x, dd y, dd z, dd w) {
   const double e2 = __fma_rn(zs, w.hi, -p2);
   double s, e3;
   two_sum(p1, p2, s, e3);
-  // low-order terms summed as a shallow tree (depth 3 instead of a 6-long chain: the dd sweep
-  // is latency-bound, ncu profiles/r01_dd_n32_ncu_full.json "wait" stalls)
-  const double t1 = __fma_rn(x.hi, y.lo, __dmul_rn(x.lo, y.hi));
-  const double t2 = __fma_rn(zs, w.lo, __dmul_rn(zl, w.hi));
-  const double t = __dadd_rn(__dadd_rn(t1, t2), __dadd_rn(__dadd_rn(e1, e2), e3));
+  double t = __dadd_rn(__dadd_rn(e1, e2), e3);
+  t = __fma_rn(x.hi, y.lo, t);
+  t = __fma_rn(x.lo, y.hi, t);
+  t = __fma_rn(zs, w.lo, t);
+  t = __fma_rn(zl, w.hi, t);
   dd r;
   two_sum(s, t, r.hi, r.lo);
   return r;
