@@ -274,7 +274,8 @@ def run_ours(args, rank, world, local_rank):
                             "units": P.units}},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "traffic_note": "dram bytes of the ncu --set full launch (2048 of the plan's units; profiles/)",
+                     "traffic_note": "dram read+write bytes of the bench's full sweep launch under ncu "
+                                     "(profiles/r01_sweep_m4_dram.csv, profiles/traffic.json)",
                      "kernel": "sweep_kernel (perm_sweep_units)", "flop_per_term": flop_per_term,
                      "fp64_instr_frac": instr_frac,
                      "peak_note": "derived FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §Roofline)",
