@@ -270,3 +270,21 @@ def test_large_n_ranges_vs_oracle(n):
         part = oracle.partial_ex(A, lo, hi, "ryser")
         got = dd_to_complex(pb.ryser_range(dA, lo, hi))
         assert abs(got - part.dd.to_complex()) <= bound_B(part, n, Pr.chunk_bits)
+
+
+# ----------------------------------------------------------------- non-finite inputs
+def test_non_finite_inputs_propagate():
+    """Input values are not checked (include/permb200.h): a NaN entry gives a NaN permanent,
+    through every path, without a fault."""
+    for n in (12, 30):
+        A = synth.gaussian(n, 3)
+        A[n // 2, n // 3] = np.nan
+        for fn in (pb.glynn, pb.ryser):
+            v = cval(fn(T(A)))
+            assert np.isnan(v.real) or np.isnan(v.imag)
+        d = pb.glynn_dd(T(A)).cpu().numpy()
+        assert np.isnan(d).any()
+    As = np.stack([synth.gaussian(8, s) for s in range(3)])
+    As[1, 0, 0] = np.inf
+    out = pb.glynn_batched(T(As)).cpu().numpy()
+    assert np.isfinite(out[0]) and np.isfinite(out[2]) and not np.isfinite(out[1])
