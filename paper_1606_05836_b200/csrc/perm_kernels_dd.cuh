@@ -80,17 +80,32 @@ constexpr int kDdChains = 4;
 // A compile-time stride lets the compiler prove that the store of row i and the load of row
 // i+1 do not alias, so the rows' independent update chains interleave.
 constexpr int kDdStride = 64;
+// n <= kDdHiRegMax: the hi halves of the row sums live in registers (4n) and only the lo halves
+// in shared memory (16 B per row per thread): half the shared memory per thread, 4 blocks of
+// 64 threads per SM instead of 3 (n = 32); one product chain keeps that within 255 registers.
+constexpr int kDdHiRegMax = 32;
+__host__ __device__ constexpr int dd_smem_parts(int N) { return N <= kDdHiRegMax ? 1 : 2; }
 
 template <int N, int ALG>
 struct DdWalker {
-  double2* ss;       // this thread's row sums: element (i, part) at ss[(2 i + part) * kDdStride]
-  dd ar, ai;         // term accumulator
-
+  static constexpr bool kHiRegs = N <= kDdHiRegMax;
+  double2* ss;
+  double2 h[kHiRegs ? N : 1];
+  dd ar, ai;
   __device__ __forceinline__ cdd load(int i) const {
+    if (kHiRegs) {
+      const double2 l = ss[i * kDdStride];
+      return cdd{dd{h[i].x, l.x}, dd{h[i].y, l.y}};
+    }
     const double2 r = ss[(2 * i) * kDdStride], m = ss[(2 * i + 1) * kDdStride];
     return cdd{dd{r.x, r.y}, dd{m.x, m.y}};
   }
   __device__ __forceinline__ void store(int i, const cdd& v) {
+    if (kHiRegs) {
+      h[i] = make_double2(v.re.hi, v.im.hi);
+      ss[i * kDdStride] = make_double2(v.re.lo, v.im.lo);
+      return;
+    }
     ss[(2 * i) * kDdStride] = make_double2(v.re.hi, v.re.lo);
     ss[(2 * i + 1) * kDdStride] = make_double2(v.im.hi, v.im.lo);
   }
@@ -98,8 +113,12 @@ struct DdWalker {
   // Row sums for code G from the row-major matrix A: Glynn s_i = a_i1 +
   // sum_{j>=2} delta_j a_ij (bit j-2 of G set <=> delta_j = -1), Ryser s_i = sum_{j in S} a_ij.
   __device__ __forceinline__ void build(const double2* __restrict__ A, uint64_t G) {
+    // kHiRegs: rows unrolled so h[i] is a register; else a runtime row loop (code size)
+#pragma unroll
+    for (int i0 = 0; i0 < (kHiRegs ? N : 1); ++i0)
 #pragma unroll 1
-    for (int i = 0; i < N; ++i) {
+    for (int i1 = 0; i1 < (kHiRegs ? 1 : N); ++i1) {
+      const int i = kHiRegs ? i0 : i1;
       const double2* row = A + i * N;
       cdd s{dd{0.0, 0.0}, dd{0.0, 0.0}};
       if (ALG == kGlynn) { const double2 v = __ldg(row); s.re.hi = v.x; s.im.hi = v.y; }
@@ -127,7 +146,7 @@ struct DdWalker {
     ai = dd{0.0, 0.0};
     double sg = 0.0;
     int col = 0;
-    constexpr int NC = N < kDdChains ? N : kDdChains;
+    constexpr int NC = (N <= kDdHiRegMax) ? 1 : (N < kDdChains ? N : kDdChains);
     for (uint64_t g = ga;;) {
       cdd c[NC];
 #pragma unroll
@@ -165,9 +184,9 @@ struct DdWalker {
 // leaf of 2^lam chunks.  Dynamic shared memory: 2 N kDdStride double2 (row sums) + blockDim
 // Dd2 (tree).
 template <int N, int ALG>
-__global__ void __launch_bounds__(kDdStride) sweep_dd_kernel(const SweepArgs args) {
+__global__ void __launch_bounds__(kDdStride, N <= kDdHiRegMax ? 4 : 1) sweep_dd_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
-  Dd2* red = reinterpret_cast<Dd2*>(smem + 2 * N * kDdStride);
+  Dd2* red = reinterpret_cast<Dd2*>(smem + dd_smem_parts(N) * N * kDdStride);
   DdWalker<N, ALG> w;
   w.ss = smem + threadIdx.x;
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(kDdStride) sweep_dd_kernel(const SweepArgs arg
 template <int N, int ALG>
 cudaError_t launch_sweep_dd(const SweepArgs& a, int64_t units, double2*, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
-  const size_t smem = sizeof(double2) * 2 * N * kDdStride + sizeof(Dd2) * threads;
+  const size_t smem = sizeof(double2) * dd_smem_parts(N) * N * kDdStride + sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(sweep_dd_kernel<N, ALG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
