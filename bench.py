@@ -294,6 +294,18 @@ def run_ours(args, rank, world, local_rank):
     }
     if cpu is not None:
         line["cpu_baseline"] = cpu
+    # The metric's third part ("n=50 permanent seconds at 8 GPUs") is not a bench step (2^49
+    # terms, 2.9 h on one GPU): it was measured once, in checkpointed sessions, by
+    # tools/m5_run.py; quoted here from its record.
+    m5 = os.path.join(ROOT, "profiles", "r01_m5_full.json")
+    if os.path.exists(m5):
+        try:
+            r = json.load(open(m5))
+            line["n50_full_run"] = {"device_seconds_1gpu": r["device_seconds"], "terms_per_s": r["terms_per_s"],
+                                    "extrapolated_8gpu_seconds": r["extrapolated_8gpu_seconds"],
+                                    "value": r["value"], "source": "profiles/r01_m5_full.json (tools/m5_run.py)"}
+        except (ValueError, KeyError, OSError):
+            pass
     print(json.dumps(line), flush=True)
     return 0
 
