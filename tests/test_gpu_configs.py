@@ -8,7 +8,9 @@ windows the oracle computes one by one, and on closed-form properties that hold 
   M3  n=32 Gaussian, Glynn + Ryser                              full value vs golden (oracle ~1 core-hour)
   M4  n=40 Haar(1600) submatrix, the bench workload             sampled canonical units vs oracle;
                                                                 block-diagonal 20+20 pin at n=40
-  M5  n=50 Gaussian                                             sampled windows vs oracle
+  M5  n=50 Gaussian                                             sampled windows (generic path) and
+                                                                fast-path units (custom plan) vs oracle;
+                                                                the full run: tools/m5_run.py
 """
 import json
 import math
@@ -124,3 +126,45 @@ def test_m5_windows_vs_oracle():
             d = fn(dA, lo, hi).cpu().numpy()
             g = complex(d[0] + d[1], d[2] + d[3])
             assert abs(g - part.dd.to_complex()) <= _bound(part, 50, P.chunk_bits), (alg, lo)
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser", "glynn_plain"])
+def test_m5_fast_path_units_vs_oracle(alg):
+    """The n = 50 FAST path (the chunk walker the M5 run and bench-style sweeps use; ranges take
+    the generic path) against the oracle: a non-canonical plan with one 2^11-term chunk per
+    unit (perm_sweep_units_custom: c = 11, leaf_bits = 0, block_bits = 0) runs the same
+    sweep_kernel<50> instantiation, so units anywhere in the Gray range can be checked one by
+    one at oracle cost."""
+    A = synth.workload("M5")
+    dA = T(A)
+    a = pb._alg(alg)
+    P = pb.plan(50, a)
+    c = 11
+    units = P.terms >> c
+    base = alg.split("_")[0]
+    for u in (0, 1, 12345678, units // 3, units - 1):
+        got = pb.sweep_units_custom(dA, a, c, 0, 0, u, u + 1).cpu().numpy()[0]
+        part = oracle.partial_ex(A, u << c, (u + 1) << c, base)
+        g = complex(got[0] + got[1], got[2] + got[3])
+        bound = _bound(part, 50, c)
+        if alg.endswith("plain"):
+            bound += U * (2 ** c + 16) * part.l1
+        assert abs(g - part.dd.to_complex()) <= bound, (alg, u, abs(g - part.dd.to_complex()) / bound)
+
+
+@pytest.mark.parametrize("n", [44, 52, 53, 56, 64])
+def test_large_n_fast_path_units_vs_oracle(n):
+    """Fast-path instantiations with the other register-budget choices (perm_kernels.cuh
+    acc_in_smem / product_chains; n >= 52 spills) on single-chunk custom units."""
+    A = synth.gaussian(n, 9300 + n)
+    dA = T(A)
+    m = n - 1
+    c, wb = 11, 7
+    lam = max(0, m - c - wb - 40)            # at most 2^40 units
+    ub = m - c - wb - lam
+    units = 1 << ub
+    for u in (0, units // 2 + 3, units - 1):
+        got = pb.sweep_units_custom(dA, pb.ALG_GLYNN, c, lam, wb, u, u + 1).cpu().numpy()[0]
+        part = oracle.partial_ex(A, u << (m - ub), (u + 1) << (m - ub))
+        g = complex(got[0] + got[1], got[2] + got[3])
+        assert abs(g - part.dd.to_complex()) <= _bound(part, n, c), (n, u)
