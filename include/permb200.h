@@ -101,12 +101,16 @@ const char* perm_strerror(int code);
 int perm_plan(int n, int alg, perm_plan_t* plan);
 
 /* ---- single permanent (device pointers) -------------------------------------------- */
+/* PAPER.md:60 (problem), Eq. (2) PAPER.md:66-68 / Alg. A2 PAPER.md:238-263 (BB/FG), Eq. (1)
+ * PAPER.md:62-64 / Alg. A1 PAPER.md:206-235 (Ryser); the final factor and the single reduction
+ * after the per-process partial sums: PAPER.md:230-232, :261-263 (reading R3: always 2^{-(N-1)}). */
 /* out[0] = Perm(A) by Eq. (2) (perm_glynn) or Eq. (1) (perm_ryser).  A: device, n*n.
  * out: device, 1 element.  = perm_sweep_units over all units + perm_combine. */
 int perm_glynn(const perm_c128* A, int n, perm_c128* out, void* stream);
 int perm_ryser(const perm_c128* A, int n, perm_c128* out, void* stream);
 
 /* ---- double-double precision mode (device pointers) -------------------------------- */
+/* Same formulas; motivated by the paper's precision finding (FIG. 4). */
 /* out[0] = Perm(A) as a complex double-double (re_hi, re_lo, im_hi, im_lo), already scaled by
  * 2^{-(N-1)} (Glynn; exact).  Same plan/tree structure as the FP64 entry points with
  * alg = PERM_ALG_GLYNN_DD / PERM_ALG_RYSER_DD.  A: device, n*n; out: device, 1 element.
@@ -115,6 +119,8 @@ int perm_glynn_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream);
 int perm_ryser_dd(const perm_c128* A, int n, perm_dd_c128* out, void* stream);
 
 /* ---- building blocks for multi-GPU partitions --------------------------------------- */
+/* The paper's per-process contiguous ranges and one ALLREDUCE (PAPER.md:204, :217-219, :230,
+ * :248-251, :261); here canonical units + a fixed reduction tree (bit-identical partitions). */
 /* Sweep kernel only: unit partials for units [unit_lo, unit_hi) of plan(n, alg), written
  * to unit_partials[0 .. unit_hi-unit_lo) (device).  One kernel launch (plus a tiny
  * column-staging kernel).  Partials are unscaled. */
@@ -146,6 +152,7 @@ int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg,
                  perm_c128* out, perm_dd_c128* out_dd, void* stream);
 
 /* ---- batched (device pointers): one permanent per thread block ---------------------- */
+/* Boson sampling needs many permanents of n x n submatrices of one unitary. */
 /* out[b] = Perm(A_b) by Eq. (2), b < batch.  A: device, batch*n*n; out: device, batch.
  * batch == 0 is a no-op returning PERM_OK. */
 int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream);
