@@ -79,6 +79,7 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
 std::once_flag g_tables_once;
 SweepLauncher g_sweep[6][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN
 SweepLauncher g_small[6][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
+FusedLauncher g_small_fused[6][kNMax + 1];   // the same + grid barrier + combine, one launch
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -104,6 +105,7 @@ void init_tables() {
     register_dd_ryser_a(g_sweep[PERM_ALG_RYSER_DD]);
     register_dd_ryser_b(g_sweep[PERM_ALG_RYSER_DD]);
     register_small(g_small);
+    register_small_fused(g_small_fused);
     register_batched_a(g_batched);
     register_batched_b(g_batched);
   });
@@ -189,27 +191,7 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
       red[tid] = plain ? plain2_add(red[tid], red[tid + o]) : dd2_add(red[tid], red[tid + o]);
     __syncthreads();
   }
-  if (tid == 0) {
-    const Dd2 r = red[0];
-    const int e = do_scale ? scale_exp : 0;
-    if (out_dd) {
-      Dd2 o = r;
-      if (scale_dd) {            // exact power-of-two scaling of both halves
-        o.re_hi = ldexp(o.re_hi, e); o.re_lo = ldexp(o.re_lo, e);
-        o.im_hi = ldexp(o.im_hi, e); o.im_lo = ldexp(o.im_lo, e);
-        if (o.re_hi == 0.0) { o.re_hi = 0.0; o.re_lo = 0.0; }   // canonical +0 (reading R11)
-        if (o.im_hi == 0.0) { o.im_hi = 0.0; o.im_lo = 0.0; }
-      }
-      *out_dd = o;
-    }
-    if (out) {
-      double re = __dadd_rn(ldexp(r.re_hi, e), ldexp(r.re_lo, e));
-      double im = __dadd_rn(ldexp(r.im_hi, e), ldexp(r.im_lo, e));
-      if (re == 0.0) re = 0.0;   // canonical +0 (reading R11)
-      if (im == 0.0) im = 0.0;
-      *out = make_double2(re, im);
-    }
-  }
+  if (tid == 0) finish_root(red[0], FinishArgs{out, out_dd, do_scale, scale_exp, scale_dd});
 }
 
 int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, Dd2* out_dd, cudaStream_t st,
@@ -288,9 +270,26 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
   double2* staging = static_cast<double2*>(ws);
   Dd2* parts = reinterpret_cast<Dd2*>(static_cast<char*>(ws) + kStagingBytes);
   const uint64_t T = 1ULL << P.log2_terms;
-  int rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
-  if (rc == PERM_OK)
-    rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), st, 1);
+  int rc;
+  init_tables();
+  if (!is_dd(alg) && P.log2_terms <= kSmallLog2 && g_small_fused[alg][n] && P.units <= (1LL << P.block_bits)) {
+    // small n: sweep + combine in one cooperative launch (same bits as the two-kernel path)
+    SweepArgs a;
+    a.A = reinterpret_cast<const double2*>(A);
+    a.unit_out = parts;
+    a.lo = 0; a.hi = T;
+    a.unit_lo = 0;
+    a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
+    a.slot = 0; a.col_base = 0; a.zero = 0;
+    const FinishArgs f{reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), is_glynn(alg) ? 1 : 0,
+                       -(n - 1), 1};
+    cudaError_t le = g_small_fused[alg][n](a, f, P.units, st);
+    rc = le == cudaSuccess ? PERM_OK : cuda_fail(le, "fused small launch");
+  } else {
+    rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
+    if (rc == PERM_OK)
+      rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), st, 1);
+  }
   cudaError_t e = cudaFreeAsync(ws, st);
   if (rc == PERM_OK && e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
   return rc;

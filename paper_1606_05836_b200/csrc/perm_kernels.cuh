@@ -25,6 +25,7 @@
 //   costs no vector register and no shared-memory bandwidth.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -541,6 +542,68 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs 
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
 }
 
+// Final step of a permanent: the unscaled root partial -> out (complex128, x 2^-(n-1) for
+// Glynn, reading R3) and/or out_dd (optionally scaled, both halves exactly); zero components
+// canonicalised to +0 (reading R11).  Shared by combine_kernel and the fused small-n kernel
+// so both produce the same bits.
+struct FinishArgs {
+  double2* out;
+  Dd2* out_dd;
+  int do_scale, scale_exp, scale_dd;
+};
+
+__device__ __forceinline__ void finish_root(const Dd2& r, const FinishArgs& f) {
+  const int e = f.do_scale ? f.scale_exp : 0;
+  if (f.out_dd) {
+    Dd2 o = r;
+    if (f.scale_dd) {            // exact power-of-two scaling of both halves
+      o.re_hi = ldexp(o.re_hi, e); o.re_lo = ldexp(o.re_lo, e);
+      o.im_hi = ldexp(o.im_hi, e); o.im_lo = ldexp(o.im_lo, e);
+      if (o.re_hi == 0.0) { o.re_hi = 0.0; o.re_lo = 0.0; }
+      if (o.im_hi == 0.0) { o.im_hi = 0.0; o.im_lo = 0.0; }
+    }
+    *f.out_dd = o;
+  }
+  if (f.out) {
+    double re = __dadd_rn(ldexp(r.re_hi, e), ldexp(r.re_lo, e));
+    double im = __dadd_rn(ldexp(r.im_hi, e), ldexp(r.im_lo, e));
+    if (re == 0.0) re = 0.0;
+    if (im == 0.0) im = 0.0;
+    *f.out = make_double2(re, im);
+  }
+}
+
+// Small-n full permanent in ONE cooperative launch: every block sweeps its unit (as
+// sweep_small_kernel), a grid barrier, then block 0 reduces the unit partials with the
+// canonical tree (units <= blockDim, a power of two: block_tree over blockDim entries with
+// zero padding pairs them exactly as combine_kernel does) and finishes.  Same bits as sweep +
+// combine, one launch fewer (M1: the combine launch measured ~5 us of a ~20 us call).
+template <int N, int ALG, bool PLAIN>
+__global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const SweepArgs args, const FinishArgs fin) {
+  extern __shared__ double2 smem[];
+  double2* at = smem;
+  double2* tab = smem + N * N;
+  Dd2* red = reinterpret_cast<Dd2*>(smem + N * N + kTabRows * N);
+  stage_transposed<N>(args.A, at, Walker<N, ALG>::kScale);
+  __syncthreads();
+  build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
+  __syncthreads();
+  const SmemColumns<N> cols{tab};
+  const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
+  const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
+  Dd2 mine;
+  if (args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  block_tree<PLAIN>(red, mine);
+  if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
+  cooperative_groups::this_grid().sync();
+  if (blockIdx.x == 0) {
+    const Dd2 v = threadIdx.x < gridDim.x ? args.unit_out[threadIdx.x] : Dd2{0.0, 0.0, 0.0, 0.0};
+    block_tree<PLAIN>(red, v);
+    if (threadIdx.x == 0) finish_root(red[0], fin);
+  }
+}
+
 // Batched Glynn: block b computes Perm(A_b) completely (boson sampling needs
 // many permanents of n x n submatrices).  Columns come from the block's shared-memory copy
 // (warp-uniform addresses: broadcast LDS).
@@ -647,6 +710,28 @@ cudaError_t launch_sweep_small(const SweepArgs& a, int64_t units, double2*, cuda
   return cudaGetLastError();
 }
 
+template <int N, int ALG, bool PLAIN>
+cudaError_t launch_sweep_small_fused(const SweepArgs& a, const FinishArgs& f, int64_t units, cudaStream_t st) {
+  const int threads = 1 << a.block_bits;
+  const size_t smem = sizeof(double2) * (N * N + kTabRows * N) + sizeof(Dd2) * threads;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(sweep_small_fused_kernel<N, ALG, PLAIN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)units);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, sweep_small_fused_kernel<N, ALG, PLAIN>, a, f);
+}
+
 template <int N>
 cudaError_t launch_batched(const BatchedArgs& a, int grid, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
@@ -675,6 +760,11 @@ void fill_sweep_plain(SweepLauncher* table, std::integer_sequence<int, Is...>) {
 template <int ALG, bool PLAIN, int LO, int... Is>
 void fill_sweep_small(SweepLauncher* table, std::integer_sequence<int, Is...>) {
   ((table[LO + Is] = &launch_sweep_small<LO + Is, ALG, PLAIN>), ...);
+}
+using FusedLauncher = cudaError_t (*)(const SweepArgs&, const FinishArgs&, int64_t units, cudaStream_t);
+template <int ALG, bool PLAIN, int LO, int... Is>
+void fill_sweep_small_fused(FusedLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_sweep_small_fused<LO + Is, ALG, PLAIN>), ...);
 }
 template <int LO, int... Is>
 void fill_batched(BatchedLauncher* table, std::integer_sequence<int, Is...>) {
