@@ -89,8 +89,8 @@ typedef struct {
 } perm_plan_t;
 
 /* Largest supported n (64 for Glynn; Ryser stops at 63 because its 2^n Gray indices
- * must fit in uint64).  n <= 56 keeps the row sums register-resident; 57..64 are correct
- * but slower (register spills). */
+ * must fit in uint64).  The FP64 sweep's hot loop is spill-free up to n = 51 (row sums in
+ * 4n registers); 52..64 are correct but slower (local-memory spills in the loop). */
 int perm_max_n(void);
 
 /* Human-readable text for a status code (for PERM_ECUDA: the last CUDA error seen by
