@@ -84,6 +84,14 @@ def main():
             fn(A)
             ms, v = ev_time(lambda: fn(A), 3)
             r[name] = {**rates(32, T, ms), "value": [v.item().real, v.item().imag]}
+        # M3 asks for the oracle timed on the box's host cores: a bounded sample of the same
+        # matrix (bench.py's cpu_oracle_rate), extrapolated to the full 2^31 terms
+        from bench import _cores, cpu_oracle_rate
+        cores = _cores()
+        rate, S, dt = cpu_oracle_rate(synth.workload("M3"), 8.0, cores)
+        r["oracle_cpu"] = {"terms_per_s": rate, "cores": cores, "sample_terms": S, "sample_seconds": dt,
+                           "glynn_full_seconds_extrapolated": (1 << 31) / rate,
+                           "gpu_over_cpu": r["glynn"]["terms_per_s"] / rate}
         res["M3"] = r
 
     if "M4" not in skip:
