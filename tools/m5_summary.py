@@ -2,6 +2,7 @@
 into the JSON kept under profiles/.
 
     python tools/m5_summary.py runs/m5 profiles/r01_m5_full.json
+    python tools/m5_summary.py runs/m5p profiles/r01_m5_plain_full.json profiles/r01_m5_full.json
 """
 import csv
 import json
@@ -18,9 +19,12 @@ def main():
     # sessions = runs of segments without a wall-clock gap above 5 minutes
     walls = [float(r["wall_time"]) for r in rows]
     sessions = 1 + sum(1 for a, b in zip(walls[:-1], walls[1:]) if b - a > 300)
+    alg = (status.get("plan") or {}).get("alg", 0)
+    mode = {0: "FP64 compensated accumulation", 4: "FP64 PLAIN accumulation (PERM_ALG_GLYNN_PLAIN)",
+            2: "double-double"}.get(alg, f"alg {alg}")
     res = {
         "config": "M5 (BASELINE.json configs[4]): n = 50 iid complex Gaussian, variance 1/n (synth.workload('M5')), "
-                  "BB/FG (Glynn), 2^49 Gray-code terms, canonical plan, ONE B200",
+                  f"BB/FG (Glynn), {mode}, 2^49 Gray-code terms, canonical plan, ONE B200",
         "complete": status.get("complete"),
         "value": status.get("value"),
         "segments": len(rows), "sessions": sessions,
@@ -36,6 +40,10 @@ def main():
                   "no oracle can walk 2^49 terms",
         "plan": status.get("plan"),
     }
+    if len(sys.argv) > 3 and res["complete"]:         # compare with another finished run (e.g. compensated)
+        other = json.load(open(sys.argv[3]))
+        v, w = complex(*res["value"]), complex(*other["value"])
+        res["rel_discrepancy_vs"] = {"file": sys.argv[3], "rel": abs(v - w) / abs(w)}
     with open(out, "w") as f:
         json.dump(res, f, indent=1)
     print(json.dumps(res, indent=1))
