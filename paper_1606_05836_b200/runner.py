@@ -117,6 +117,8 @@ def run_checkpointed(A: torch.Tensor, alg="glynn", prefix: Optional[str] = None,
     # claim counter for this run: a fresh key per call (rank 0 draws the run id)
     key = None
     if world > 1:
+        # the default group's rendezvous store (torchrun's TCPStore); pass `store` explicitly to
+        # avoid this private accessor
         store = store or dist.distributed_c10d._get_default_store()
         ids = [int(store.add(f"permb200/run/{sha[:16]}/{a}", 1)) if rank == 0 else 0]
         dist.broadcast_object_list(ids, src=0, group=group)
