@@ -23,10 +23,10 @@ import torch
 import oracle
 import synth
 import paper_1606_05836_b200 as pb
+from tolerance import U, check_B, check_R
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
-U = 2.0 ** -53
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
@@ -39,18 +39,14 @@ def _dd(hexes):
     return complex(v[0] + v[1], v[2] + v[3])
 
 
-def _bound(part, n, c, scale=1.0):
-    return U * ((math.sqrt(n) + 2 ** (c / 2)) * part.l1c + (3 * n + 16) * part.l1) * scale
-
-
 def test_m1_glynn_ryser():
     A = synth.workload("M1")
     ref = oracle.glynn(A).value
     g = complex(pb.glynn(T(A)).item())
-    assert abs(g - ref) <= 1e-9 * abs(ref)
+    check_R(g, ref, what="M1 glynn")
     part = oracle.partial_ex(A, 0, 1 << 20, "ryser")
     r = complex(pb.ryser(T(A)).item())
-    assert abs(r - ref) <= 1e-9 * abs(ref) or abs(r - part.dd.to_complex()) <= _bound(part, 20, pb.plan(20, 1).chunk_bits)
+    check_B(r, part, 20, pb.plan(20, 1).chunk_bits, rel_ceiling=1e-3, what="M1 ryser")
 
 
 def test_m2_batched_all_4096_vs_golden():
@@ -99,7 +95,7 @@ def test_m4_sampled_units_vs_oracle():
         got = pb.sweep_units(dA, pb.ALG_GLYNN, u, u + 1).cpu().numpy()[0]
         part = oracle.partial_ex(A, u * P.unit_terms, (u + 1) * P.unit_terms)
         g = complex(got[0] + got[1], got[2] + got[3])
-        assert abs(g - part.dd.to_complex()) <= _bound(part, 40, P.chunk_bits), u
+        check_B(g, part, 40, P.chunk_bits, what=f"M4 unit {u}")
 
 
 @pytest.mark.slow
@@ -125,7 +121,7 @@ def test_m5_windows_vs_oracle():
             part = oracle.partial_ex(A, lo, hi, alg)
             d = fn(dA, lo, hi).cpu().numpy()
             g = complex(d[0] + d[1], d[2] + d[3])
-            assert abs(g - part.dd.to_complex()) <= _bound(part, 50, P.chunk_bits), (alg, lo)
+            check_B(g, part, 50, P.chunk_bits, what=f"M5 {alg} window {lo}")
 
 
 @pytest.mark.parametrize("alg", ["glynn", "ryser", "glynn_plain"])
@@ -146,10 +142,8 @@ def test_m5_fast_path_units_vs_oracle(alg):
         got = pb.sweep_units_custom(dA, a, c, 0, 0, u, u + 1).cpu().numpy()[0]
         part = oracle.partial_ex(A, u << c, (u + 1) << c, base)
         g = complex(got[0] + got[1], got[2] + got[3])
-        bound = _bound(part, 50, c)
-        if alg.endswith("plain"):
-            bound += U * (2 ** c + 16) * part.l1
-        assert abs(g - part.dd.to_complex()) <= bound, (alg, u, abs(g - part.dd.to_complex()) / bound)
+        extra = U * (2 ** c + 16) * part.l1 if alg.endswith("plain") else 0.0
+        check_B(g, part, 50, c, extra=extra, what=f"M5 {alg} unit {u}")
 
 
 @pytest.mark.parametrize("n", [44, 52, 53, 56, 64])
@@ -167,4 +161,4 @@ def test_large_n_fast_path_units_vs_oracle(n):
         got = pb.sweep_units_custom(dA, pb.ALG_GLYNN, c, lam, wb, u, u + 1).cpu().numpy()[0]
         part = oracle.partial_ex(A, u << (m - ub), (u + 1) << (m - ub))
         g = complex(got[0] + got[1], got[2] + got[3])
-        assert abs(g - part.dd.to_complex()) <= _bound(part, n, c), (n, u)
+        check_B(g, part, n, c, what=f"n={n} unit {u}")

@@ -24,10 +24,10 @@ import torch
 import oracle
 import synth
 import paper_1606_05836_b200 as pb
+from tolerance import U_DD, bound_dd, check_B, check_R
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
-U_DD = 2.0 ** -104
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
@@ -42,10 +42,6 @@ def exact_dd(t) -> tuple[Fraction, Fraction]:
 
 def cdd(t) -> complex:
     return pb.dd_to_complex(t.cpu().numpy())
-
-
-def bound_dd(part, n: int, c: int, scale: float = 1.0) -> float:
-    return 2 * U_DD * ((math.sqrt(n) + 2 ** (c / 2)) * part.l1c + (3 * n + 32) * part.l1) * scale
 
 
 # ----------------------------------------------------------------- Edd (bit-exact)
@@ -101,8 +97,8 @@ def test_dd_gaussian_vs_oracle(n, alg):
     scale = 2.0 ** -(n - 1) if alg == "glynn" else 1.0
     ref = part.dd.scaled(-(n - 1)).to_complex() if alg == "glynn" else part.dd.to_complex()
     got = cdd((pb.glynn_dd if alg == "glynn" else pb.ryser_dd)(T(A)))
-    assert abs(got - ref) <= 1e-9 * abs(ref)
-    assert abs(got - ref) <= bound_dd(part, n, P.chunk_bits, scale) + 1e-300, (abs(got - ref), bound_dd(part, n, P.chunk_bits, scale))
+    check_R(got, ref, what=f"{alg}_dd n={n}")
+    check_B(got, part, n, P.chunk_bits, scale, ref=ref, dd=True, rel_ceiling=1e-20, what=f"{alg}_dd n={n}")
 
 
 @pytest.mark.parametrize("alg", ["glynn", "ryser"])
@@ -150,7 +146,7 @@ def test_dd_ranges_ragged(alg):
     for lo, hi in list(zip(cuts[:-1], cuts[1:])) + [(0, P.terms), (5, P.terms - 3)]:
         part = oracle.partial_ex(A, lo, hi, alg[:5])
         got = cdd(pb.range_partial(dA, a, lo, hi))
-        assert abs(got - part.dd.to_complex()) <= bound_dd(part, n, P.chunk_bits) + 1e-300, (lo, hi)
+        check_B(got, part, n, P.chunk_bits, dd=True, what=f"{alg} [{lo},{hi})")
 
 
 @pytest.mark.parametrize("n,alg", [(20, "glynn_dd"), (21, "ryser_dd")])
@@ -186,7 +182,7 @@ def test_dd_large_n_windows(n):
         for lo, hi in [(0, 2 * chunk), (P.terms - chunk - 77, P.terms)]:
             part = oracle.partial_ex(A, lo, hi, alg[:5])
             got = cdd(pb.range_partial(dA, a, lo, hi))
-            assert abs(got - part.dd.to_complex()) <= bound_dd(part, n, P.chunk_bits), (alg, lo)
+            check_B(got, part, n, P.chunk_bits, dd=True, what=f"{alg} n={n} [{lo},{hi})")
 
 
 def test_dd_m4_sampled_units_vs_oracle():
@@ -197,7 +193,7 @@ def test_dd_m4_sampled_units_vs_oracle():
         got = pb.sweep_units(dA, pb.ALG_GLYNN_DD, u, u + 1).cpu().numpy()[0]
         part = oracle.partial_ex(A, u * P.unit_terms, (u + 1) * P.unit_terms)
         g = complex(got[0] + got[1], got[2] + got[3])
-        assert abs(g - part.dd.to_complex()) <= bound_dd(part, 40, P.chunk_bits), u
+        check_B(g, part, 40, P.chunk_bits, dd=True, what=f"M4 dd unit {u}")
 
 
 def test_dd_bad_arguments():

@@ -20,10 +20,10 @@ import torch
 import oracle
 import synth
 import paper_1606_05836_b200 as pb
+from tolerance import U, bound_B, check_B, check_R  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
-U = 2.0 ** -53
 
 
 def T(a):
@@ -86,26 +86,22 @@ def _rel(a: complex, b: complex) -> float:
     return abs(a - b) / abs(b)
 
 
-def bound_B(part: "oracle.Partial", n: int, c: int, scale: float = 1.0) -> float:
-    return U * ((math.sqrt(n) + 2 ** (c / 2)) * part.l1c + (3 * n + 16) * part.l1) * scale
-
-
 @pytest.mark.parametrize("n", list(range(1, 21)) + [22, 24])
 def test_class_R_gaussian_glynn(n):
     A = synth.gaussian(n, 2000 + n)
     ref = oracle.glynn(A)
     got = cval(pb.glynn(T(A)))
-    assert _rel(got, ref.value) <= 1e-9, (_rel(got, ref.value), got, ref.value)
+    check_R(got, ref.value, what=f"glynn n={n}")
     P = pb.plan(n)
     part = oracle.partial_ex(A, 0, P.terms)
-    assert abs(got - ref.value) <= bound_B(part, n, P.chunk_bits, 2.0 ** -(n - 1))
+    check_B(got, part, n, P.chunk_bits, 2.0 ** -(n - 1), ref=ref.value, rel_ceiling=1e-7, what=f"glynn n={n}")
 
 
 @pytest.mark.parametrize("seed", range(6))
 def test_class_R_gaussian_n20_seeds(seed):
     A = synth.gaussian(20, 1000 + seed)
     ref = oracle.glynn(A)
-    assert _rel(cval(pb.glynn(T(A))), ref.value) <= 1e-9
+    check_R(cval(pb.glynn(T(A))), ref.value, what=f"seed {seed}")
 
 
 @pytest.mark.parametrize("n", [16, 20, 24])
@@ -129,8 +125,9 @@ def test_ryser_R_or_B(n):
     part = oracle.partial_ex(A, 0, P.terms, "ryser")
     ref = part.dd.to_complex()
     got = cval(pb.ryser(T(A)))
-    bound = bound_B(part, n, P.chunk_bits)
-    assert _rel(got, ref) <= 1e-9 or abs(got - ref) <= bound, (_rel(got, ref), abs(got - ref) / bound)
+    # R or B (the paper's finding: FP64 Ryser cannot always meet 1e-9); B is always checked and
+    # its bound stays below 1e-3 |ref| (measured worst 1.5e-5 at n = 22)
+    check_B(got, part, n, P.chunk_bits, rel_ceiling=1e-3, what=f"ryser n={n} (rel {_rel(got, ref):.1e})")
 
 
 # ----------------------------------------------------------------- ranges, ragged ends, partitions
@@ -147,7 +144,7 @@ def test_range_partials_ragged(alg):
     for lo, hi in list(zip(cuts[:-1], cuts[1:])) + [(0, Tn), (3, Tn - 7), (Tn - 1, Tn)]:
         part = oracle.partial_ex(A, lo, hi, alg)
         got = dd_to_complex(fn(dA, lo, hi))
-        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, c) + 1e-300, (lo, hi)
+        check_B(got, part, n, c, what=f"{alg} [{lo},{hi})")
     assert dd_to_complex(fn(dA, 9, 9)) == 0
 
 
@@ -263,13 +260,13 @@ def test_large_n_ranges_vs_oracle(n):
     for lo, hi in [(0, 4 * chunk), (P.terms - 3 * chunk - 5, P.terms), (7 * chunk + 3, 9 * chunk + 1)]:
         part = oracle.partial_ex(A, lo, hi)
         got = dd_to_complex(pb.glynn_range(dA, lo, hi))
-        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, P.chunk_bits), (lo, hi)
+        check_B(got, part, n, P.chunk_bits, what=f"glynn n={n} [{lo},{hi})")
     if n <= 63:
         Pr = pb.plan(n, pb.ALG_RYSER)
         lo, hi = Pr.terms - 2 * chunk, Pr.terms
         part = oracle.partial_ex(A, lo, hi, "ryser")
         got = dd_to_complex(pb.ryser_range(dA, lo, hi))
-        assert abs(got - part.dd.to_complex()) <= bound_B(part, n, Pr.chunk_bits)
+        check_B(got, part, n, Pr.chunk_bits, what=f"ryser n={n} [{lo},{hi})")
 
 
 # ----------------------------------------------------------------- non-finite inputs

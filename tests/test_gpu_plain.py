@@ -16,20 +16,14 @@ import torch
 import oracle
 import synth
 import paper_1606_05836_b200 as pb
+from tolerance import check_B, plain_extra
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda:0")
-U = 2.0 ** -53
 
 
 def T(a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128)).to(DEV)
-
-
-def bound_plain(part, P, scale=1.0):
-    b = (math.sqrt(P.n) + 2 ** (P.chunk_bits / 2)) * part.l1c + (3 * P.n + 16) * part.l1
-    k = 2 ** (P.chunk_bits + P.leaf_bits) + P.block_bits + P.unit_bits + 16
-    return U * (b + k * part.l1) * scale
 
 
 @pytest.mark.parametrize("alg", ["glynn", "ryser"])
@@ -42,7 +36,7 @@ def test_plain_vs_oracle(n, alg):
     scale = 2.0 ** -(n - 1) if alg == "glynn" else 1.0
     ref = part.dd.to_complex() * scale
     got = complex(pb.perm_alg(T(A), a).item())
-    assert abs(got - ref) <= bound_plain(part, P, scale) + 1e-300, (abs(got - ref), bound_plain(part, P, scale))
+    check_B(got, part, n, P.chunk_bits, scale, ref=ref, extra=plain_extra(part, P, scale), what=f"{alg}_plain n={n}")
 
 
 @pytest.mark.parametrize("alg", ["glynn", "ryser"])

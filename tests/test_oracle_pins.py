@@ -329,3 +329,130 @@ def test_paper_diag_1pi_45_term_identity():
     d = oracle.glynn_partial(A, lo, hi, threads=2)[0]
     assert d.exact() == (Fraction(-(hi - lo) * 2 ** 22), Fraction(-(hi - lo) * 2 ** 22))
     assert (1 + 1j) ** 45 == complex(-2 ** 22, -2 ** 22)
+
+
+# ----------------------------------------------------------------- error scales L1 and L1c
+# oracle.partial_ex returns, besides the value, the two error scales every class-B tolerance
+# is built from (reading R10b; tests/tolerance.py):
+#   L1  = sum over the walked terms of |term|
+#   L1c = sum over the walked terms of |term| * sum_i (sum_j |a_ij|) / |s_i|
+# (s_i the row sums of that term).  Pinned here against closed forms and an independent
+# brute-force enumeration (ascending delta / subset order, numpy arithmetic, no Gray walk),
+# so a mistake in them cannot silently loosen or tighten the GPU parity checks.
+
+def _l1_closed_J(n: int, alg: str) -> tuple[int, Fraction]:
+    """J_n: Glynn terms with k of delta_2..delta_n = -1 have every row sum n - 2k (C(n-1, k) of
+    them); Ryser subsets of size k have every row sum k (C(n, k) of them).  Row abs sum = n."""
+    l1, l1c = 0, Fraction(0)
+    if alg == "glynn":
+        for k in range(n):
+            s = abs(n - 2 * k)
+            l1 += math.comb(n - 1, k) * s ** n
+            if s:
+                l1c += math.comb(n - 1, k) * Fraction(s ** n * n * n, s)
+    else:
+        for k in range(1, n + 1):
+            l1 += math.comb(n, k) * k ** n
+            l1c += math.comb(n, k) * Fraction(k ** n * n * n, k)
+    return l1, l1c
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+@pytest.mark.parametrize("n", [1, 2, 5, 9, 14, 20])
+def test_error_scales_J_closed_form(n, alg):
+    T = 1 << (n - 1 if alg == "glynn" else n)
+    part = oracle.partial_ex(synth.ones(n), 0, T, alg)
+    l1, l1c = _l1_closed_J(n, alg)
+    tol = T * 2.0 ** -53 + 1e-14          # the scales are plain FP64 sums over T terms
+    assert part.l1 == pytest.approx(float(l1), rel=tol)
+    assert part.l1c == pytest.approx(float(l1c), rel=tol)
+    if alg == "glynn" and n > 1:
+        # the 2^-(n-1) scale is applied to L1 where glynn() applies it to the value
+        assert oracle.glynn(synth.ones(n)).l1 == pytest.approx(float(l1) / 2 ** (n - 1), rel=tol)
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+@pytest.mark.parametrize("n", [1, 4, 11, 30])
+def test_error_scales_diag_closed_form(n, alg):
+    """diag(d), d_i != 0: Glynn row sums are delta_i d_i, every one of the 2^(n-1) terms has
+    modulus prod |d_i| and kappa = sum_i |d_i| / |d_i| = n;  Ryser: only S = all columns gives a
+    non-zero term.  So L1c = n L1 exactly in both."""
+    rng = np.random.default_rng(n)
+    d = (rng.uniform(0.5, 2.0, n) * np.exp(1j * rng.uniform(0, 2 * np.pi, n)))
+    A = np.diag(d)
+    T = 1 << (n - 1 if alg == "glynn" else n)
+    lo, hi = 0, T
+    if T > 1 << 20 and alg == "glynn":
+        lo, hi = T - (1 << 16), T
+    elif T > 1 << 20:
+        # a window holding the full set for Ryser: Gray index g with G(g) = 2^n - 1
+        g, code = 0, (1 << n) - 1
+        while code:
+            g ^= code
+            code >>= 1
+        lo, hi = max(0, g - (1 << 15)), min(T, g + (1 << 15))
+    part = oracle.partial_ex(A, lo, hi, alg)
+    prod = float(np.prod(np.abs(d)))
+    want = (hi - lo) * prod if alg == "glynn" else prod
+    assert part.l1 == pytest.approx(want, rel=1e-12)
+    assert part.l1c == pytest.approx(n * want, rel=1e-12)
+
+
+@pytest.mark.parametrize("A,alg", [(synth.ones_minus_eye(9), "glynn"), (synth.ones_minus_eye(9), "ryser"),
+                                   (synth.bernoulli(12, 2), "glynn"), (synth.bernoulli(12, 2), "ryser"),
+                                   (synth.random_int(10, 3, complex_=False), "glynn")],
+                         ids=["J-I9g", "J-I9r", "bern12g", "bern12r", "rint10g"])
+def test_error_scales_L1_equals_exact_int(A, alg):
+    """On real integer matrices the exact-int128 oracle's L1 (sum |Re t| + |Im t|) is the
+    walk's L1 (sum |t|), computed independently and exactly."""
+    n = A.shape[0]
+    T = 1 << (n - 1 if alg == "glynn" else n)
+    part = oracle.partial_ex(A, 0, T, alg)
+    ex = oracle.exact(A, alg)
+    assert part.l1 == pytest.approx(float(ex.l1), rel=1e-13)
+
+
+def _brute_scales(A, alg):
+    """Independent enumeration (ascending delta / subset index, numpy complex arithmetic)."""
+    n = A.shape[0]
+    rowabs = np.abs(A).sum(axis=1)
+    l1 = l1c = 0.0
+    if alg == "glynn":
+        for m in range(1 << (n - 1)):
+            delta = np.array([1.0] + [-1.0 if (m >> (j - 1)) & 1 else 1.0 for j in range(1, n)])
+            s = A @ delta
+            t = abs(np.prod(s))
+            l1 += t
+            if t > 0:
+                l1c += t * float(np.sum(rowabs / np.abs(s)))
+    else:
+        for m in range(1 << n):
+            sel = np.array([1.0 if (m >> j) & 1 else 0.0 for j in range(n)])
+            s = A @ sel
+            t = abs(np.prod(s))
+            l1 += t
+            if t > 0:
+                l1c += t * float(np.sum(rowabs / np.abs(s)))
+    return l1, l1c
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+@pytest.mark.parametrize("n,seed", [(3, 1), (6, 2), (9, 3)])
+def test_error_scales_bruteforce(n, seed, alg):
+    A = synth.gaussian(n, 700 + seed)
+    T = 1 << (n - 1 if alg == "glynn" else n)
+    part = oracle.partial_ex(A, 0, T, alg)
+    l1, l1c = _brute_scales(A, alg)
+    assert part.l1 == pytest.approx(l1, rel=1e-10)
+    assert part.l1c == pytest.approx(l1c, rel=1e-10)
+    # every row sum is bounded by its row's abs sum, so each kappa term is >= n
+    assert part.l1c >= n * part.l1 * (1 - 1e-12)
+
+
+def test_error_scales_additive_over_ranges():
+    """L1 and L1c of a range are sums over its terms: additive over any split."""
+    A = synth.gaussian(12, 5)
+    full = oracle.partial_ex(A, 0, 1 << 11)
+    a, b = oracle.partial_ex(A, 0, 777), oracle.partial_ex(A, 777, 1 << 11)
+    assert a.l1 + b.l1 == pytest.approx(full.l1, rel=1e-13)
+    assert a.l1c + b.l1c == pytest.approx(full.l1c, rel=1e-13)
