@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "m5"))
     ap.add_argument("--budget-s", type=float, default=1700.0)
     ap.add_argument("--segment-units", type=int, default=2368)
+    ap.add_argument("--max-segments", type=int, default=None, help="stop after this many segments (tests)")
     ap.add_argument("--session", default=None, help="tag of this session's ledger (default: a timestamp)")
     a = ap.parse_args()
     t_start = time.monotonic()
@@ -112,7 +113,7 @@ def main():
 
     deadline = t_start + a.budget_s
     val, done = run_checkpointed(A, alg, os.path.join(work, f"m5_{a.alg}"), segment_units=a.segment_units,
-                                 deadline=deadline, sweep=sweep, on_segment=on_segment, store=store, tag=session)
+                                 deadline=deadline, max_segments=a.max_segments, sweep=sweep, on_segment=on_segment, store=store, tag=session)
     fh.close()
     for f in glob.glob(os.path.join(work, f"*.rank{rank}.{session}.*")):   # this session's ledger + log
         shutil.copy(f, a.out)
