@@ -8,9 +8,12 @@ Workload (BASELINE.json configs[3], "M4"): one 40 x 40 complex128 submatrix of a
 over 2^39 Gray-code terms, partitioned over the N GPUs of one node (strong scaling: the
 total work is fixed) with one NCCL all_reduce.  One step = one full permanent.
 
-Under torchrun (N > 1) every rank runs its share; the per-step device time is the max over
-ranks.  Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (the only
-reference this paper-tier task has) on the host cores; under torchrun only rank 0 works.
+`--gpus N` (N > 1) without torchrun re-launches itself through torch.distributed.run with N
+ranks (fails loudly if fewer than N GPUs are visible; PERMB200_DIST_BACKEND=gloo runs the
+N-rank logic with ranks sharing GPUs).  Every rank runs its share; the per-step device time
+is the max over ranks; NCCL_DEBUG=INFO (INIT) puts the communicator init in the log.  Rank 0
+prints ONE JSON line.  --impl reference times the CPU oracle (the only reference this
+paper-tier task has) on the host cores; under torchrun only rank 0 works.
 """
 from __future__ import annotations
 
@@ -156,7 +159,21 @@ def run_reference(args, rank, world):
     return 0
 
 
-def run_ours(args, rank, world, local_rank):
+def _ncu_fp64_pipe(n: int):
+    """FP64-pipe utilisation of the sweep kernel from the latest committed ncu summary
+    (profiles/r0*_sweep_n<n>*_ncu_full.json), or None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", f"r0*_sweep_n{n}*ncu_full.json")), reverse=True):
+        try:
+            m = json.load(open(path))["metrics"]
+            return {"pct": float(m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"][1]),
+                    "source": os.path.relpath(path, ROOT)}
+        except (ValueError, KeyError, OSError):
+            continue
+    return None
+
+
+def run_ours(args, rank, world, local_rank, shared_gpu: bool):
     import torch
     import torch.distributed as dist
 
@@ -175,25 +192,22 @@ def run_ours(args, rank, world, local_rank):
     A_pinned = torch.from_numpy(A_np).pin_memory()
     ulo, uhi = pdist.unit_range(P.units, world, rank)
     my_terms = (uhi - ulo) * P.unit_terms
+    aligned = pdist.subtree_aligned(P.units, world)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     stream = torch.cuda.current_stream(dev)
     sweep_ms = []
 
     def step(time_sweep: bool):
-        # one full permanent: sweep my units -> subtree root -> one all_reduce -> combine
+        # one full permanent: sweep my units -> (world > 1: one collective) -> combine + scale
         if time_sweep:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
         parts = pb.sweep_units(A, alg, ulo, uhi)
         if time_sweep:
             e1.record(stream)
-        root = pb.combine(parts, n, alg, scale=False)[1]
-        roots = pdist.gather_roots(root, world, rank)
-        val, _ = pb.combine(roots, n, alg, scale=True)
-        if time_sweep:
             sweep_ms.append((e0, e1))
-        return val
+        return pdist.reduce_partials(parts, n, alg, P.units, ulo, uhi, world, rank)
 
     def barrier():
         if world > 1:
@@ -208,6 +222,7 @@ def run_ours(args, rank, world, local_rank):
     clocks.start()
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    k0 = pb.launch_count()
     t_start.record(stream)
     for k in range(args.steps):
         v = step(True)
@@ -215,16 +230,25 @@ def run_ours(args, rank, world, local_rank):
             flush.zero_()        # L2 flushed between timed steps
     t_end.record(stream)
     barrier()
+    launches = pb.launch_count() - k0
     clk = clocks.stop()
     ms_total = t_start.elapsed_time(t_end)
     sweep_avg = float(np.mean([a.elapsed_time(b) for a, b in sweep_ms]))
     value_c = complex(v.item())
     mx = torch.tensor([ms_total, sweep_avg], dtype=torch.float64, device=dev)
+    nl = torch.tensor([launches], dtype=torch.int64, device=dev)
+    clocks_all = [clk]
     if world > 1:
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nl, op=dist.ReduceOp.SUM)
+        clocks_all = [None] * world
+        dist.all_gather_object(clocks_all, clk)
     ms_total, sweep_max = float(mx[0]), float(mx[1])
+    launches_all = int(nl[0])
 
-    # end to end through the public API with host buffers (C-ABI perm_glynn_host at N=1)
+    # end to end through the public API with host buffers: the C-ABI perm_glynn_host at N = 1;
+    # at N > 1 the pinned host matrix is copied to every GPU inside the timed region, then
+    # perm_dist, and the result is read back to the host
     e2e_ms = []
     for k in range(max(1, args.e2e_steps)):
         barrier()
@@ -263,51 +287,94 @@ def run_ours(args, rank, world, local_rank):
         rate, S, dt = cpu_oracle_rate(A_np, args.cpu_seconds, cores)
         cpu = {"value": rate, "unit": "terms/s", "cores": cores, "kind": "oracle",
                "sample": f"first {S} of 2^{n - 1} Gray indices of the same matrix, double-double oracle, {dt:.1f} s"}
+    if world == 1:
+        par = "single GPU: sweep + canonical combine, no collective"
+    elif aligned:
+        par = (f"Gray-index range partition over {world} GPUs: per-rank subtree root, one "
+               f"{'gloo' if shared_gpu else 'NCCL'} all_reduce of the ({world}, 4) root table")
+    else:
+        par = (f"Gray-index range partition over {world} GPUs: one {'gloo' if shared_gpu else 'NCCL'} "
+               f"all_reduce of the ({P.units}, 4) unit-partial table")
     line = {
         "metric": "BB/FG Gray-code terms/s", "value": value, "unit": "terms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {synth.WORKLOADS[args.workload]['desc']}", "n": n,
                    "terms": terms, "l2": "flushed between timed steps (256 MiB write)",
-                   "parallelism": f"Gray-index range partition over {world} GPU(s), one NCCL all_reduce",
+                   "parallelism": par,
                    "plan": {"chunk_bits": P.chunk_bits, "leaf_bits": P.leaf_bits, "block_bits": P.block_bits,
                             "units": P.units}},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "traffic_note": "dram read+write bytes of the bench's full sweep launch under ncu "
-                                     "(profiles/r01_sweep_m4_dram.csv, profiles/traffic.json)",
                      "kernel": "sweep_kernel (perm_sweep_units)", "flop_per_term": flop_per_term,
+                     "fp64_pipe_pct_ncu": _ncu_fp64_pipe(n),
                      "fp64_instr_frac": instr_frac,
-                     "peak_note": "derived FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md §Roofline)",
-                     "measured_peak": FP64_MEASURED_TFLOPS,
-                     "frac_of_measured": achieved / FP64_MEASURED_TFLOPS,
-                     "fp64_issue_frac_of_measured": instr_frac * FP64_PEAK_TFLOPS / FP64_MEASURED_TFLOPS,
-                     "measured_peak_note": "sustained DFMA microbenchmark, profiles/r01_fp64_probe.log; "
-                                           "algorithmic ceiling (8n-4)/(2(6n-2)) = 0.664 of any DFMA peak"},
-        "e2e": {"value": terms / (e2e_ms_step * 1e-3), "unit": "terms/s", "h2d_bytes_per_step": 16 * n * n,
-                "d2h_bytes_per_step": 16, "ms_per_step": e2e_ms_step},
-        "gpu_launches": 4 * args.steps,
-        "clocks": clk,
+                     "algorithmic_ceiling": flop_per_term / (2 * fp64_instr_per_term),
+                     "peak_note": "nominal FP64 FMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (MEASURED_PEAKS.json has "
+                                  "no FP64 entry); a term needs 6n-2 FP64 instructions for 8n-4 flops, so "
+                                  "frac <= algorithmic_ceiling; fp64_instr_frac and ncu's FP64-pipe % are the "
+                                  "utilisation figures",
+                     "traffic_note": "dram read+write bytes of one full sweep launch, kernel-only ncu capture "
+                                     "(profiles/traffic.json); algorithmic bytes 16n^2 in + 32 B per unit out",
+                     "builder_dfma_probe_tflops": FP64_MEASURED_TFLOPS,
+                     "builder_dfma_probe_note": "the builder's DFMA microbenchmark (profiles/r01_fp64_probe.log); "
+                                                "the sweep issues as fast as it, so it understates the pipe peak"},
+        "e2e": {"value": terms / (e2e_ms_step * 1e-3), "unit": "terms/s", "h2d_bytes_per_step": 16 * n * n * world,
+                "d2h_bytes_per_step": 16 * world, "ms_per_step": e2e_ms_step,
+                "path": "C-ABI perm_glynn_host" if world == 1 else "pinned host -> each GPU, dist.perm_dist, .item()"},
+        "gpu_launches": launches_all,
+        "gpu_launches_note": f"libpermb200 kernels in the timed region, all ranks (perm_launch_count): "
+                             f"{launches_all // max(1, args.steps)} per step",
+        "clocks": clocks_all[0],
         "result": [value_c.real, value_c.imag],
         "paper_context": {"tianhe2_bbfg_hybrid_256_nodes_n40_s": 132.35, "derived_terms_per_s": 4.15e9,
                           "cite": "PAPER.md:562 (Table preTestBBFG)"},
     }
+    if world > 1:
+        line["clocks_per_rank"] = clocks_all
+        if shared_gpu:
+            line["ranks_share_gpus"] = True
     if cpu is not None:
         line["cpu_baseline"] = cpu
     # The metric's third part ("n=50 permanent seconds at 8 GPUs") is not a bench step (2^49
-    # terms, 2.9 h on one GPU): it was measured once, in checkpointed sessions, by
-    # tools/m5_run.py; quoted here from its record.
+    # terms, 2.9 h on one GPU): it was measured once on ONE GPU, in checkpointed sessions, by
+    # tools/m5_run.py; quoted here from its record, with the 8-GPU figure labelled as the
+    # linear extrapolation it is.
     m5 = os.path.join(ROOT, "profiles", "r01_m5_full.json")
     if os.path.exists(m5):
         try:
             r = json.load(open(m5))
             line["n50_full_run"] = {"device_seconds_1gpu": r["device_seconds"], "terms_per_s": r["terms_per_s"],
-                                    "extrapolated_8gpu_seconds": r["extrapolated_8gpu_seconds"],
-                                    "value": r["value"], "source": "profiles/r01_m5_full.json (tools/m5_run.py)"}
+                                    "linear_extrapolation_8gpu_seconds": r["device_seconds"] / 8,
+                                    "value": r["value"], "measured_on": "1 GPU",
+                                    "source": "profiles/r01_m5_full.json (tools/m5_run.py)"}
         except (ValueError, KeyError, OSError):
             pass
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _self_launch(args) -> int:
+    """`bench.py --gpus N` without torchrun: re-launch this script as N ranks through
+    torch.distributed.run on 127.0.0.1 (the driver's command shape), with the NCCL init log on."""
+    import socket
+    import torch
+    backend = os.environ.get("PERMB200_DIST_BACKEND", "nccl")
+    have = torch.cuda.device_count()
+    if args.impl == "ours" and backend == "nccl" and have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have} "
+                         f"(set PERMB200_DIST_BACKEND=gloo to run the N-rank logic on shared GPUs)\n")
+        return 2
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -323,22 +390,39 @@ def main():
     args = ap.parse_args()
     if args.workload == "M2":
         raise SystemExit("M2 is a batched parity config; bench the single-permanent workloads")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return _self_launch(args)
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local_rank = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    import torch
+    backend = os.environ.get("PERMB200_DIST_BACKEND", "nccl")
+    need = world if backend == "nccl" else 1
+    if torch.cuda.device_count() < need:
+        sys.stderr.write(f"bench.py: {world} rank(s) on backend {backend} needs {need} visible GPUs, found "
+                         f"{torch.cuda.device_count()}\n")
+        return 2
+    shared_gpu = False
     if world > 1:
         import torch
         import torch.distributed as dist
         backend = os.environ.get("PERMB200_DIST_BACKEND", "nccl")    # gloo: CPU-side test of the N>1 logic
         if backend == "nccl":
+            if torch.cuda.device_count() < world:
+                raise SystemExit(f"bench.py: {world} ranks need {world} GPUs, found {torch.cuda.device_count()}")
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # the communicator init (nRanks) in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local_rank)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
+            shared_gpu = torch.cuda.device_count() < world
     try:
-        return run_ours(args, rank, world, local_rank)
+        return run_ours(args, rank, world, local_rank, shared_gpu)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -35,6 +35,17 @@
  * safe (the per-device constant-memory column slots are fenced with events).
  * Functions suffixed _host take HOST pointers and are synchronous.
  *
+ * Deliberate deviations from SURVEY §8(b)'s conventions (measured trade-offs):
+ *   - "no persistent library allocations": the library keeps a per-device stream-ordered
+ *     memory pool (release threshold 256 MiB) for its workspaces -- the default pool remapped
+ *     pages on every synchronous call (4.2 ms instead of tens of us for n = 20);
+ *   - "no __constant__ matrix symbol": FP64 sweeps of more than 2^21 terms stage the signed
+ *     column table in a per-translation-unit __constant__ slot so every column operand is a
+ *     uniform-register LDCU read (this is what holds the FP64 pipe at ~90 %).  Consequences:
+ *     such sweeps on one device serialise across streams (event-fenced slot reuse), and they
+ *     refuse CUDA-graph capture (PERM_ECUDA); small n, the dd mode and the batched kernel use
+ *     shared memory and are concurrent and capturable.
+ *
  * Errors: every function returns PERM_OK (0) or an error code; nothing is written on
  * PERM_EINVAL.  Asynchronous device faults surface at the caller's next synchronisation.
  * Input VALUES are not checked: NaN / Inf propagate.  Results never contain -0.0.
@@ -68,8 +79,14 @@ enum {
  * paper's "Perm = Perm +- delta" -- for the precision lab's
  * compensated-vs-plain accumulation discrepancy.  Same terms, same order,
  * same speed; partials carry lo = 0 and perm_combine adds them in plain FP64. */
+/* *_SEP: the paper's "separate addition" summation order (Table AV):
+ * the terms of even and of odd Gray index (even / odd |S|, resp. number of delta = -1) are
+ * summed separately in plain FP64 and subtracted once at the end.  Partials carry the even
+ * sum in the hi slots and the odd sum in the lo slots (re_hi = sum_even Re, re_lo = sum_odd
+ * Re, ...); perm_combine adds them componentwise and finishes with (even - odd) times
+ * (-1)^n (Ryser) / 2^{-(n-1)} (Glynn).  Precision-lab mode, n <= 40. */
 enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_RYSER_DD = 3,
-       PERM_ALG_GLYNN_PLAIN = 4, PERM_ALG_RYSER_PLAIN = 5 };
+       PERM_ALG_GLYNN_PLAIN = 4, PERM_ALG_RYSER_PLAIN = 5, PERM_ALG_GLYNN_SEP = 6, PERM_ALG_RYSER_SEP = 7 };
 
 /* The canonical evaluation plan for (n, alg).  It depends only on (n, alg), never on
  * the GPU count, so any partition of the unit range reproduces the single-GPU result
@@ -157,10 +174,33 @@ int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg,
  * batch == 0 is a no-op returning PERM_OK. */
 int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream);
 
+/* out[b] = |Perm(A_b)|^2, the boson-sampling probability numerator P(S|T) ~ |Perm(U_ST)|^2
+ * (FIG. 1), computed in the kernel from the rounded permanent as
+ * fma(re, re, im * im).  out: device, batch doubles.  Otherwise as perm_glynn_batched. */
+int perm_glynn_batched_abs2(const perm_c128* A, int n, int64_t batch, double* out, void* stream);
+
+/* ---- summation-order experiments (precision lab, Table AV) --- */
+/* out[0] = (partials[order[0]] + partials[order[1]] + ... + partials[order[count-1]]) added
+ * SEQUENTIALLY in plain FP64 in the given order (each partial first rounded to hi + lo), times
+ * 2^{-(n-1)} for Glynn algs.  With the chunk partials of a plain-mode sweep (e.g.
+ * perm_sweep_units_custom with chunk_bits 5, leaf_bits 0, block_bits 0: 32-term chunks) and a
+ * random permutation as `order`, this is the paper's "random order" summation at 32-term
+ * granularity; the identity order is its "original order".  partials, order: device; order
+ * must be a permutation of [0, count) (not checked: device data).  One thread adds (the
+ * order IS the experiment); count < 1 or null pointers -> PERM_EINVAL. */
+int perm_sum_ordered(const perm_dd_c128* partials, int64_t count, const int64_t* order, int n, int alg,
+                     perm_c128* out, void* stream);
+
 /* ---- host-buffer entry points (synchronous; copies inside) -------------------------- */
 int perm_glynn_host(const perm_c128* A, int n, perm_c128* out);
 int perm_ryser_host(const perm_c128* A, int n, perm_c128* out);
 int perm_glynn_batched_host(const perm_c128* A, int n, int64_t batch, perm_c128* out);
+int perm_glynn_batched_abs2_host(const perm_c128* A, int n, int64_t batch, double* out);
+
+/* ---- instrumentation ------------------------------------------------------------------ */
+/* Number of CUDA kernels this library has launched since it was loaded (all devices and
+ * threads; the column-staging kernel counts).  bench.py reads it around its timed region. */
+long long perm_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -25,13 +25,15 @@ from typing import Optional
 import torch
 
 from . import _lib
-from ._lib import (ALG_GLYNN, ALG_GLYNN_DD, ALG_GLYNN_PLAIN, ALG_RYSER, ALG_RYSER_DD, ALG_RYSER_PLAIN,  # noqa: F401
-                   Plan, PermError, max_n, plan)
+from ._lib import (ALG_GLYNN, ALG_GLYNN_DD, ALG_GLYNN_PLAIN, ALG_GLYNN_SEP, ALG_RYSER, ALG_RYSER_DD,  # noqa: F401
+                   ALG_RYSER_PLAIN, ALG_RYSER_SEP, Plan, PermError, launch_count, max_n, plan)
 
 __all__ = ["glynn", "ryser", "glynn_batched", "glynn_range", "ryser_range", "sweep_units", "combine",
            "glynn_host", "ryser_host", "glynn_batched_host", "plan", "max_n", "Plan", "PermError",
-           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "ALG_GLYNN_PLAIN", "ALG_RYSER_PLAIN", "glynn_dd", "ryser_dd", "range_partial", "perm_alg", "sweep_units_custom", "PermGraph",
-           "dd_to_complex"]
+           "ALG_GLYNN", "ALG_RYSER", "ALG_GLYNN_DD", "ALG_RYSER_DD", "ALG_GLYNN_PLAIN", "ALG_RYSER_PLAIN",
+           "ALG_GLYNN_SEP", "ALG_RYSER_SEP", "glynn_dd", "ryser_dd", "range_partial", "perm_alg", "sweep_units_custom",
+           "PermGraph", "dd_to_complex", "glynn_batched_abs2", "glynn_batched_abs2_host", "sum_ordered",
+           "launch_count"]
 
 
 def _stream(device: torch.device) -> int:
@@ -59,6 +61,10 @@ def _alg(alg) -> int:
         return ALG_GLYNN_PLAIN
     if alg in (ALG_RYSER_PLAIN, "ryser_plain"):
         return ALG_RYSER_PLAIN
+    if alg in (ALG_GLYNN_SEP, "glynn_sep"):
+        return ALG_GLYNN_SEP
+    if alg in (ALG_RYSER_SEP, "ryser_sep"):
+        return ALG_RYSER_SEP
     raise ValueError(f"unknown algorithm {alg!r}")
 
 
@@ -107,18 +113,52 @@ def dd_to_complex(d) -> complex:
     return complex(v[0] + v[1], v[2] + v[3])
 
 
-def glynn_batched(As: torch.Tensor) -> torch.Tensor:
-    """(B, n, n) complex128 CUDA -> (B,) permanents, one thread block per matrix."""
+def _batch(As: torch.Tensor) -> tuple[int, int]:
     if not isinstance(As, torch.Tensor) or As.dtype != torch.complex128 or not As.is_cuda:
         raise TypeError("expected a torch.complex128 CUDA tensor")
     if As.dim() != 3 or As.shape[1] != As.shape[2]:
         raise ValueError(f"expected (B, n, n), got {tuple(As.shape)}")
-    B, n = As.shape[0], As.shape[1]
+    return As.shape[0], As.shape[1]
+
+
+def glynn_batched(As: torch.Tensor) -> torch.Tensor:
+    """(B, n, n) complex128 CUDA -> (B,) permanents, one thread block per matrix."""
+    B, n = _batch(As)
     As = As.contiguous()
     out = torch.empty((B,), dtype=torch.complex128, device=As.device)
     with torch.cuda.device(As.device):
         _lib.check(_lib.lib().perm_glynn_batched(As.data_ptr() if B else None, n, B, out.data_ptr() if B else None,
                                                  _stream(As.device)), "perm_glynn_batched")
+    return out
+
+
+def glynn_batched_abs2(As: torch.Tensor) -> torch.Tensor:
+    """(B, n, n) complex128 CUDA -> (B,) float64 |Perm(A_b)|^2 (boson-sampling probability
+    numerators), computed in the batched kernel."""
+    B, n = _batch(As)
+    As = As.contiguous()
+    out = torch.empty((B,), dtype=torch.float64, device=As.device)
+    with torch.cuda.device(As.device):
+        _lib.check(_lib.lib().perm_glynn_batched_abs2(As.data_ptr() if B else None, n, B,
+                                                      out.data_ptr() if B else None, _stream(As.device)),
+                   "perm_glynn_batched_abs2")
+    return out
+
+
+def sum_ordered(partials: torch.Tensor, order: torch.Tensor, n: int, alg) -> torch.Tensor:
+    """Sequential plain-FP64 sum of (count, 4) float64 CUDA partials in the order given by the
+    int64 CUDA permutation `order`, finished like perm_combine (x 2^-(n-1) for Glynn): the
+    paper's "original" / "random" summation orders (Table AV; perm_sum_ordered)."""
+    if partials.dtype != torch.float64 or not partials.is_cuda or partials.dim() != 2 or partials.shape[1] != 4:
+        raise TypeError("expected a (count, 4) float64 CUDA tensor")
+    if order.dtype != torch.int64 or order.device != partials.device or order.shape != (partials.shape[0],):
+        raise TypeError("order must be an int64 tensor of shape (count,) on the partials' device")
+    partials, order = partials.contiguous(), order.contiguous()
+    out = torch.empty((), dtype=torch.complex128, device=partials.device)
+    with torch.cuda.device(partials.device):
+        _lib.check(_lib.lib().perm_sum_ordered(partials.data_ptr(), partials.shape[0], order.data_ptr(), int(n),
+                                               _alg(alg), out.data_ptr(), _stream(partials.device)),
+                   "perm_sum_ordered")
     return out
 
 
@@ -218,24 +258,48 @@ def _host(fn, name, A, n, batch) -> "object":
     return out
 
 
-def glynn_host(A) -> complex:
-    """Host-buffer entry point (C ABI perm_glynn_host): numpy in, complex out; copies inside."""
+def _host_square(A):
     import numpy as np
     a = np.ascontiguousarray(A, dtype=np.complex128)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or a.shape[0] < 1:
+        raise ValueError(f"expected a square matrix, got shape {a.shape}")
+    return a
+
+
+def _host_batch(As):
+    import numpy as np
+    a = np.ascontiguousarray(As, dtype=np.complex128)
+    if a.ndim != 3 or a.shape[1] != a.shape[2] or a.shape[1] < 1:
+        raise ValueError(f"expected (B, n, n), got shape {a.shape}")
+    return a
+
+
+def glynn_host(A) -> complex:
+    """Host-buffer entry point (C ABI perm_glynn_host): numpy in, complex out; copies inside."""
+    a = _host_square(A)
     return complex(_host(_lib.lib().perm_glynn_host, "perm_glynn_host", a, a.shape[0], None)[0])
 
 
 def ryser_host(A) -> complex:
-    import numpy as np
-    a = np.ascontiguousarray(A, dtype=np.complex128)
+    a = _host_square(A)
     return complex(_host(_lib.lib().perm_ryser_host, "perm_ryser_host", a, a.shape[0], None)[0])
 
 
 def glynn_batched_host(As):
-    import numpy as np
-    a = np.ascontiguousarray(As, dtype=np.complex128)
+    a = _host_batch(As)
     B, n = a.shape[0], a.shape[1]
     return _host(_lib.lib().perm_glynn_batched_host, "perm_glynn_batched_host", a, n, B)[:B]
+
+
+def glynn_batched_abs2_host(As):
+    """Host-buffer |Perm(A_b)|^2 (C ABI perm_glynn_batched_abs2_host): (B,) float64."""
+    import numpy as np
+    a = _host_batch(As)
+    B, n = a.shape[0], a.shape[1]
+    out = np.empty(max(B, 1), dtype=np.float64)
+    _lib.check(_lib.lib().perm_glynn_batched_abs2_host(a.ctypes.data, n, B, out.ctypes.data),
+               "perm_glynn_batched_abs2_host")
+    return out[:B]
 
 
 class PermGraph:

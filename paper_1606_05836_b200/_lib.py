@@ -13,12 +13,14 @@ LIB_PATH = os.path.join(_HERE, "libpermb200.so")
 
 PERM_OK, PERM_EINVAL, PERM_ECUDA, PERM_ENOTIMPL = 0, 1, 2, 3
 ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD, ALG_GLYNN_PLAIN, ALG_RYSER_PLAIN = 0, 1, 2, 3, 4, 5
+ALG_GLYNN_SEP, ALG_RYSER_SEP = 6, 7
 
 # every symbol include/permb200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "perm_max_n", "perm_strerror", "perm_plan", "perm_glynn", "perm_ryser", "perm_sweep_units",
     "perm_glynn_range", "perm_ryser_range", "perm_combine", "perm_glynn_batched", "perm_glynn_host",
     "perm_ryser_host", "perm_glynn_batched_host", "perm_glynn_dd", "perm_ryser_dd", "perm_range", "perm_sweep_units_custom",
+    "perm_glynn_batched_abs2", "perm_glynn_batched_abs2_host", "perm_sum_ordered", "perm_launch_count",
 )
 
 
@@ -83,9 +85,14 @@ def lib() -> ctypes.CDLL:
         L.perm_glynn_host.argtypes = [vp, i32, vp]
         L.perm_ryser_host.argtypes = [vp, i32, vp]
         L.perm_glynn_batched_host.argtypes = [vp, i32, i64, vp]
+        L.perm_glynn_batched_abs2.argtypes = [vp, i32, i64, vp, vp]
+        L.perm_glynn_batched_abs2_host.argtypes = [vp, i32, i64, vp]
+        L.perm_sum_ordered.argtypes = [vp, i64, vp, i32, i32, vp, vp]
+        L.perm_launch_count.argtypes = []
         for name in EXPORTS:
-            if name not in ("perm_max_n", "perm_strerror"):
+            if name not in ("perm_max_n", "perm_strerror", "perm_launch_count"):
                 getattr(L, name).restype = i32
+        L.perm_launch_count.restype = ctypes.c_longlong
         _lib = L
     return _lib
 
@@ -108,3 +115,8 @@ def plan(n: int, alg: int = ALG_GLYNN) -> Plan:
     check(lib().perm_plan(int(n), int(alg), ctypes.byref(p)), "perm_plan")
     return Plan(p.n, p.alg, p.log2_terms, p.chunk_bits, p.leaf_bits, p.block_bits, p.unit_bits,
                 int(p.unit_terms), int(p.units))
+
+
+def launch_count() -> int:
+    """Kernels libpermb200.so has launched since it was loaded (perm_launch_count)."""
+    return int(lib().perm_launch_count())

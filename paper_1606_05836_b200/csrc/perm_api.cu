@@ -6,6 +6,7 @@
 // pairwise tree (combine kernel) -> x 2^-(n-1) exactly once (reading R3).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -17,6 +18,10 @@ using namespace permb200;
 namespace {
 
 thread_local std::string g_last_error;
+
+// Kernels this library has launched (all devices, all threads): perm_launch_count().
+std::atomic<long long> g_launches{0};
+inline void note_launch(int k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 int cuda_fail(cudaError_t e, const char* where) {
   g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
@@ -77,9 +82,10 @@ cudaError_t ws_alloc(void** p, size_t bytes, cudaStream_t st) {
 }
 
 std::once_flag g_tables_once;
-SweepLauncher g_sweep[6][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN
-SweepLauncher g_small[6][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
-FusedLauncher g_small_fused[6][kNMax + 1];   // the same + grid barrier + combine, one launch
+constexpr int kAlgs = 8;
+SweepLauncher g_sweep[kAlgs][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN, GLYNN_SEP, RYSER_SEP
+SweepLauncher g_small[kAlgs][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
+FusedLauncher g_small_fused[kAlgs][kNMax + 1];   // the same + grid barrier + combine, one launch
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -104,6 +110,10 @@ void init_tables() {
     register_dd_glynn_b(g_sweep[PERM_ALG_GLYNN_DD]);
     register_dd_ryser_a(g_sweep[PERM_ALG_RYSER_DD]);
     register_dd_ryser_b(g_sweep[PERM_ALG_RYSER_DD]);
+    register_sep_glynn_a(g_sweep[PERM_ALG_GLYNN_SEP]);
+    register_sep_glynn_b(g_sweep[PERM_ALG_GLYNN_SEP]);
+    register_sep_ryser_a(g_sweep[PERM_ALG_RYSER_SEP]);
+    register_sep_ryser_b(g_sweep[PERM_ALG_RYSER_SEP]);
     register_small(g_small);
     register_small_fused(g_small_fused);
     register_batched_a(g_batched);
@@ -117,11 +127,17 @@ int ceil_log2(long long v) {
   return k;
 }
 
-bool valid_alg(int alg) { return alg >= PERM_ALG_GLYNN && alg <= PERM_ALG_RYSER_PLAIN; }
-// alg = formula (bit 0: 0 Glynn, 1 Ryser) + 2 * arithmetic mode (0 FP64, 1 dd, 2 plain FP64)
+bool valid_alg(int alg) { return alg >= PERM_ALG_GLYNN && alg <= PERM_ALG_RYSER_SEP; }
+// alg = formula (bit 0: 0 Glynn, 1 Ryser) + 2 * arithmetic mode (0 FP64, 1 dd, 2 plain FP64,
+// 3 separate addition)
 bool is_glynn(int alg) { return (alg & 1) == 0; }
 bool is_plain(int alg) { return alg == PERM_ALG_GLYNN_PLAIN || alg == PERM_ALG_RYSER_PLAIN; }
 bool is_dd(int alg) { return alg == PERM_ALG_GLYNN_DD || alg == PERM_ALG_RYSER_DD; }
+bool is_sep(int alg) { return alg == PERM_ALG_GLYNN_SEP || alg == PERM_ALG_RYSER_SEP; }
+// accumulation mode of the FP64 sweep / combine (perm_kernels.cuh kComp / kPlain / kSep)
+int mode_of(int alg) { return is_plain(alg) ? kPlain : is_sep(alg) ? kSep : kComp; }
+// the one subtraction of separate addition: even - odd, times (-1)^n for Ryser (Eq. (1))
+int sep_sign(int n, int alg) { return !is_sep(alg) ? 0 : (!is_glynn(alg) && (n & 1)) ? -1 : 1; }
 
 void make_plan(int n, int alg, perm_plan_t* p) {
   const int m = is_glynn(alg) ? n - 1 : n;
@@ -160,14 +176,18 @@ void make_plan(int n, int alg, perm_plan_t* p) {
 }
 
 bool valid_n(int n) { return n >= 1 && n <= kNMax; }
-// Ryser has 2^n terms: n = 64 would overflow the 64-bit Gray index.
-bool valid_n_alg(int n, int alg) { return valid_alg(alg) && valid_n(n) && (is_glynn(alg) ? true : n <= 63); }
+// Ryser has 2^n terms: n = 64 would overflow the 64-bit Gray index.  The separate-addition
+// precision mode is compiled for n <= kSepNMax (the paper's Table AV stops at N = 32).
+constexpr int kSepNMax = 40;
+bool valid_n_alg(int n, int alg) {
+  return valid_alg(alg) && valid_n(n) && (is_glynn(alg) ? true : n <= 63) && (!is_sep(alg) || n <= kSepNMax);
+}
 
 // Canonical tree over `count` partials (zero-padded to P = 2^k): one block of up to 1024
 // threads; thread t reduces the aligned segment [t*S, (t+1)*S) with the binary-counter
 // method (node = left + right), then a pairwise tree over the segment roots in smem.
 __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int64_t P, int do_scale,
-                               int scale_exp, double2* out, Dd2* out_dd, int scale_dd, int plain) {
+                               int scale_exp, double2* out, Dd2* out_dd, int scale_dd, int mode, int sep) {
   __shared__ Dd2 red[1024];
   const int64_t T = P < 1024 ? P : 1024;
   const int64_t S = P / T;
@@ -179,7 +199,10 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
       const int64_t idx = tid * S + k;
       Dd2 v = idx < count ? parts[idx] : Dd2{0.0, 0.0, 0.0, 0.0};
       int lvl = 0;
-      for (int64_t kk = k; kk & 1; kk >>= 1) { v = plain ? plain2_add(stack[lvl], v) : dd2_add(stack[lvl], v); ++lvl; }
+      for (int64_t kk = k; kk & 1; kk >>= 1) {
+        v = mode == kPlain ? plain2_add(stack[lvl], v) : mode == kSep ? sep2_add(stack[lvl], v) : dd2_add(stack[lvl], v);
+        ++lvl;
+      }
       stack[lvl] = v;
       if (lvl > top_level) top_level = lvl;
     }
@@ -188,18 +211,59 @@ __global__ void combine_kernel(const Dd2* __restrict__ parts, int64_t count, int
   __syncthreads();
   for (int64_t o = 1; o < T; o <<= 1) {
     if ((tid & (2 * o - 1)) == 0 && tid + o < T)
-      red[tid] = plain ? plain2_add(red[tid], red[tid + o]) : dd2_add(red[tid], red[tid + o]);
+      red[tid] = mode == kPlain ? plain2_add(red[tid], red[tid + o])
+                 : mode == kSep ? sep2_add(red[tid], red[tid + o]) : dd2_add(red[tid], red[tid + o]);
     __syncthreads();
   }
-  if (tid == 0) finish_root(red[0], FinishArgs{out, out_dd, do_scale, scale_exp, scale_dd});
+  if (tid == 0) finish_root(red[0], FinishArgs{out, out_dd, do_scale, scale_exp, scale_dd, sep});
+}
+
+// Sequential plain-FP64 sum of `count` partials in a caller-given order (the paper's "original"
+// and "random" summation orders, Table AV): the order is the point, so the additions
+// form ONE dependent chain.  Warp 1 gathers batches of 1024 partials (rounded hi + lo) into a
+// double-buffered shared-memory tile while thread 0 adds the previous batch in order.
+__global__ void __launch_bounds__(64) ordered_sum_kernel(const Dd2* __restrict__ parts,
+                                                         const int64_t* __restrict__ order, int64_t count,
+                                                         FinishArgs f) {
+  constexpr int B = 1024;
+  __shared__ double2 buf[2][B];
+  const int tid = threadIdx.x;
+  const int64_t nb = (count + B - 1) / B;
+  auto load = [&](int64_t b, int slot) {
+    for (int k = tid - 32; k < B; k += 32) {
+      const int64_t idx = b * B + k;
+      double2 v = make_double2(0.0, 0.0);
+      if (idx < count) {
+        const Dd2 p = parts[order[idx]];
+        v = make_double2(__dadd_rn(p.re_hi, p.re_lo), __dadd_rn(p.im_hi, p.im_lo));
+      }
+      buf[slot][k] = v;
+    }
+  };
+  if (tid >= 32 && nb > 0) load(0, 0);
+  __syncthreads();
+  double sr = 0.0, si = 0.0;
+  for (int64_t b = 0; b < nb; ++b) {
+    if (tid >= 32) {
+      if (b + 1 < nb) load(b + 1, (int)((b + 1) & 1));
+    } else if (tid == 0) {
+      const int m = (int)(count - b * B < B ? count - b * B : B);
+      const double2* t = buf[b & 1];
+      for (int k = 0; k < m; ++k) { sr = __dadd_rn(sr, t[k].x); si = __dadd_rn(si, t[k].y); }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) finish_root(Dd2{sr, 0.0, si, 0.0}, f);
 }
 
 int run_combine(const Dd2* parts, int64_t count, int n, int alg, double2* out, Dd2* out_dd, cudaStream_t st,
                 int scale_dd = 0) {
   int64_t P = 1;
   while (P < count) P <<= 1;
-  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, is_glynn(alg), -(n - 1), out, out_dd, scale_dd, is_plain(alg));
+  combine_kernel<<<1, 1024, 0, st>>>(parts, count, P, is_glynn(alg), -(n - 1), out, out_dd, scale_dd, mode_of(alg),
+                                     sep_sign(n, alg));
   CUDA_TRY(cudaGetLastError(), "combine_kernel launch");
+  note_launch();
   return PERM_OK;
 }
 
@@ -221,6 +285,7 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
     // small n: columns from shared memory, no staging / constant slot / fencing
     a.slot = 0; a.col_base = 0;
     CUDA_TRY(g_small[P.alg][P.n](a, u_hi - u_lo, staging, st), "small sweep launch");
+    note_launch();
     return PERM_OK;
   }
   {
@@ -237,6 +302,7 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   if (is_dd(P.alg)) {            // the dd sweep reads its columns from A: no constant slot
     a.slot = 0; a.col_base = 0;
     CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "dd sweep launch");
+    note_launch();
     return PERM_OK;
   }
   DeviceSlots& ds = g_slots[dev];
@@ -252,6 +318,7 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   a.slot = slot;
   a.col_base = slot * kTabRows * kNMax;
   CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "sweep launch");
+  note_launch(a.c >= 5 ? 2 : 1);         // column staging (c >= 5) + sweep
   CUDA_TRY(cudaEventRecord(ds.ev[slot], st), "cudaEventRecord");
   ds.used[slot] = true;
   return PERM_OK;
@@ -282,9 +349,10 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
     a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
     a.slot = 0; a.col_base = 0; a.zero = 0;
     const FinishArgs f{reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), is_glynn(alg) ? 1 : 0,
-                       -(n - 1), 1};
+                       -(n - 1), 1, sep_sign(n, alg)};
     cudaError_t le = g_small_fused[alg][n](a, f, P.units, st);
     rc = le == cudaSuccess ? PERM_OK : cuda_fail(le, "fused small launch");
+    if (rc == PERM_OK) note_launch();
   } else {
     rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
     if (rc == PERM_OK)
@@ -430,31 +498,57 @@ int perm_combine(const perm_dd_c128* partials, int64_t count, int n, int alg, pe
                      reinterpret_cast<Dd2*>(out_dd), static_cast<cudaStream_t>(stream));
 }
 
-int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream) {
+static int batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, double* out_abs2, void* stream) {
   if (!valid_n(n) || batch < 0) return PERM_EINVAL;
   if (batch == 0) return PERM_OK;
-  if (!A || !out) return PERM_EINVAL;
+  if (!A || (!out && !out_abs2)) return PERM_EINVAL;
   init_tables();
   BatchedArgs a;
   a.A = reinterpret_cast<const double2*>(A);
   a.out = reinterpret_cast<double2*>(out);
+  a.out_abs2 = out_abs2;
   a.batch = batch;
   make_batched_plan(n, &a.block_bits, &a.c, &a.lam);
   a.scale_exp = -(n - 1);
   a.zero = 0;
   const int grid = batch < (1LL << 30) ? (int)batch : (1 << 30);
   CUDA_TRY(g_batched[n](a, grid, static_cast<cudaStream_t>(stream)), "batched launch");
+  note_launch();
   return PERM_OK;
 }
 
-static int host_call(const perm_c128* A, int n, int64_t batch, perm_c128* out, int which) {
+int perm_glynn_batched(const perm_c128* A, int n, int64_t batch, perm_c128* out, void* stream) {
+  if (!out && batch > 0) return PERM_EINVAL;
+  return batched(A, n, batch, out, nullptr, stream);
+}
+
+int perm_glynn_batched_abs2(const perm_c128* A, int n, int64_t batch, double* out, void* stream) {
+  if (!out && batch > 0) return PERM_EINVAL;
+  return batched(A, n, batch, nullptr, out, stream);
+}
+
+int perm_sum_ordered(const perm_dd_c128* partials, int64_t count, const int64_t* order, int n, int alg,
+                     perm_c128* out, void* stream) {
+  if (!partials || !order || !out || count < 1 || !valid_n_alg(n, alg)) return PERM_EINVAL;
+  const FinishArgs f{reinterpret_cast<double2*>(out), nullptr, is_glynn(alg) ? 1 : 0, -(n - 1), 0, 0};
+  ordered_sum_kernel<<<1, 64, 0, static_cast<cudaStream_t>(stream)>>>(reinterpret_cast<const Dd2*>(partials),
+                                                                        order, count, f);
+  CUDA_TRY(cudaGetLastError(), "ordered_sum_kernel launch");
+  note_launch();
+  return PERM_OK;
+}
+
+long long perm_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+static int host_call(const perm_c128* A, int n, int64_t batch, void* out, int which) {
   if (!A || !out || !valid_n(n) || batch < 0) return PERM_EINVAL;
   if (batch == 0) return PERM_OK;
   cudaStream_t st = nullptr;
   CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
   void* dA = nullptr;
   void* dO = nullptr;
-  const size_t abytes = sizeof(perm_c128) * (size_t)n * n * batch, obytes = sizeof(perm_c128) * batch;
+  const size_t abytes = sizeof(perm_c128) * (size_t)n * n * batch;
+  const size_t obytes = (which == 3 ? sizeof(double) : sizeof(perm_c128)) * batch;
   int rc = PERM_OK;
   cudaError_t e = ws_alloc(&dA, abytes, st);
   if (e == cudaSuccess) e = ws_alloc(&dO, obytes, st);
@@ -465,7 +559,8 @@ static int host_call(const perm_c128* A, int n, int64_t batch, perm_c128* out, i
     perm_c128* o = static_cast<perm_c128*>(dO);
     if (which == 0) rc = perm_glynn(a, n, o, st);
     else if (which == 1) rc = perm_ryser(a, n, o, st);
-    else rc = perm_glynn_batched(a, n, batch, o, st);
+    else if (which == 2) rc = perm_glynn_batched(a, n, batch, o, st);
+    else rc = perm_glynn_batched_abs2(a, n, batch, static_cast<double*>(dO), st);
   }
   if (rc == PERM_OK) {
     e = cudaMemcpyAsync(out, dO, obytes, cudaMemcpyDeviceToHost, st);
@@ -483,6 +578,9 @@ int perm_glynn_host(const perm_c128* A, int n, perm_c128* out) { return host_cal
 int perm_ryser_host(const perm_c128* A, int n, perm_c128* out) { return host_call(A, n, 1, out, 1); }
 int perm_glynn_batched_host(const perm_c128* A, int n, int64_t batch, perm_c128* out) {
   return host_call(A, n, batch, out, 2);
+}
+int perm_glynn_batched_abs2_host(const perm_c128* A, int n, int64_t batch, double* out) {
+  return host_call(A, n, batch, out, 3);
 }
 
 }  // extern "C"

@@ -33,6 +33,15 @@ namespace permb200 {
 
 enum { kGlynn = 0, kRyser = 1 };
 
+// Accumulation modes of the FP64 sweep (template parameter MODE):
+//   kComp  compensated: 16-term plain sums -> Sum2 cascade -> double-double partials (default)
+//   kPlain plain FP64 everywhere, the paper's "Perm = Perm +- delta" (reading R12)
+//   kSep   the paper's "separate addition" (Table AV): the terms of even and
+//          of odd Gray index (|S| / number of -1 in delta even or odd) are summed separately in
+//          plain FP64 -- partials carry (even, odd) in the (hi, lo) slots -- and subtracted once,
+//          at the very end (finish_root).
+enum { kComp = 0, kPlain = 1, kSep = 2 };
+
 constexpr int kNMax = 64;      // largest n
 constexpr int kCMax = 12;      // largest chunk_bits
 constexpr int kTabBits = 16;   // Gray bits covered by a column table (rows for bits >= c are zero)
@@ -57,7 +66,8 @@ struct SweepArgs {
 
 struct BatchedArgs {
   const double2* A;      // device, batch * n*n
-  double2* out;          // device, batch
+  double2* out;          // device, batch (nullptr: |perm|^2 only)
+  double* out_abs2;      // device, batch: |perm|^2 (boson-sampling probability numerator) or nullptr
   int64_t batch;
   int c, lam, block_bits;
   int scale_exp;         // -(n-1)
@@ -169,23 +179,31 @@ __device__ __forceinline__ Dd2 plain2_add(const Dd2& a, const Dd2& b) {
   return Dd2{__dadd_rn(a.re_hi, b.re_hi), 0.0, __dadd_rn(a.im_hi, b.im_hi), 0.0};
 }
 
-template <bool PLAIN>
+// Separate-addition partials (kSep): (even, odd) sums in the (hi, lo) slots, each added in
+// plain FP64 on its own.
+__device__ __forceinline__ Dd2 sep2_add(const Dd2& a, const Dd2& b) {
+  return Dd2{__dadd_rn(a.re_hi, b.re_hi), __dadd_rn(a.re_lo, b.re_lo), __dadd_rn(a.im_hi, b.im_hi),
+             __dadd_rn(a.im_lo, b.im_lo)};
+}
+
+template <int MODE>
 __device__ __forceinline__ Dd2 part_add(const Dd2& a, const Dd2& b) {
-  return PLAIN ? plain2_add(a, b) : dd2_add(a, b);
+  return MODE == kComp ? dd2_add(a, b) : MODE == kPlain ? plain2_add(a, b) : sep2_add(a, b);
 }
 
 // ------------------------------------------------------------------ the walker
-// PLAIN = false: compensated accumulation (Sum2 cascade + dd partials, the default);
-// PLAIN = true: every accumulation in plain FP64 (the precision lab's "plain" mode, §8(f)2:
-// same terms, same order, only the compensation removed).
-template <int N, int ALG, bool PLAIN = false, bool SMEM_ACC = acc_in_smem(N)>
+// MODE = kComp: compensated accumulation (Sum2 cascade + dd partials, the default);
+// kPlain: every accumulation in plain FP64 (the precision lab's "plain" mode, §8(f)2: same
+// terms, same order, only the compensation removed); kSep: even / odd terms summed apart.
+template <int N, int ALG, int MODE = kComp, bool SMEM_ACC = acc_in_smem(N)>
 struct Walker {
+  static constexpr bool PLAIN = (MODE == kPlain);
   double2 s[N];                  // row sums (registers)
   // Cascaded (Sum2) double-double accumulator of the chunk (PLAIN: hi halves only): in
   // registers, or (acc_in_smem(N)) in this thread's shared-memory slot, which the kernels place
   // right after their N*N matrix copy and blockDim reduction entries.
   static constexpr bool kSmemAcc = SMEM_ACC;
-  double arh, arl, aih, ail;
+  double arh, arl, aih, ail;     // kSep: arh/aih even sums, arl/ail odd sums
   Dd2* accs;
 
   // Column sources hold STEP VECTORS u = kScale * column (Glynn 2a: exact doubling; Ryser a).
@@ -205,6 +223,19 @@ struct Walker {
     } else {
       arh = arl = aih = ail = 0.0;
     }
+  }
+
+  // kSep: the even-g and odd-g block sums enter their own plain accumulators.
+  __device__ __forceinline__ void acc_add_sep(double er, double ei, double orr, double oi) {
+    if (kSmemAcc) {
+      Dd2 a = *accs;
+      a.re_hi = __dadd_rn(a.re_hi, er); a.re_lo = __dadd_rn(a.re_lo, orr);
+      a.im_hi = __dadd_rn(a.im_hi, ei); a.im_lo = __dadd_rn(a.im_lo, oi);
+      *accs = a;
+      return;
+    }
+    arh = __dadd_rn(arh, er); arl = __dadd_rn(arl, orr);
+    aih = __dadd_rn(aih, ei); ail = __dadd_rn(ail, oi);
   }
 
   __device__ __forceinline__ void acc_add(double re, double im) {
@@ -305,7 +336,8 @@ struct Walker {
   // fall back to per-thread LDC + spills (tests/test_build_sass.py guards this).
   template <class Cols>
   __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero) {
-    double mr = 0.0, mi = 0.0;
+    double mr = 0.0, mi = 0.0;      // kSep: even-g block sums
+    double orr = 0.0, oi = 0.0;     // kSep only: odd-g block sums
     for (int t = -4; t < H - 4; t += 4) {
       const int tz = t * zero;
 #pragma unroll
@@ -315,12 +347,20 @@ struct Walker {
         const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
         flip_row(cols, row);
         const double2 p = row_product<N>(s);
-        if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
+        if (MODE == kSep) {          // parity of g = parity of r (T0 and t + 4 are multiples of 4)
+          if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
+          else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
+        } else if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
         else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
       }
-      if (((t + 4) & 12) == 12) { acc_add(mr, mi); mr = 0.0; mi = 0.0; }
+      if (((t + 4) & 12) == 12) {
+        if (MODE == kSep) { acc_add_sep(mr, mi, orr, oi); orr = 0.0; oi = 0.0; }
+        else acc_add(mr, mi);
+        mr = 0.0; mi = 0.0;
+      }
     }
-    acc_add(mr, mi);
+    if (MODE == kSep) acc_add_sep(mr, mi, orr, oi);
+    else acc_add(mr, mi);
   }
 
   // Full aligned chunk q (Gray indices [q 2^c, (q+1) 2^c)), c >= 5.
@@ -346,9 +386,14 @@ struct Walker {
     build(at, ga ^ (ga >> 1));
     for (uint64_t g = ga;; ) {
       double2 p = row_product<N>(s);
-      const bool neg = ((g & 1) != 0) != kNegBase;
-      if (neg) { p.x = -p.x; p.y = -p.y; }
-      acc_add(p.x, p.y);
+      if (MODE == kSep) {
+        if (g & 1) acc_add_sep(0.0, 0.0, p.x, p.y);
+        else acc_add_sep(p.x, p.y, 0.0, 0.0);
+      } else {
+        const bool neg = ((g & 1) != 0) != kNegBase;
+        if (neg) { p.x = -p.x; p.y = -p.y; }
+        acc_add(p.x, p.y);
+      }
       if (++g >= gb) break;
       const int b = __ffsll((long long)g) - 1;
       const double sg = ((g >> (b + 1)) & 1) ? kSgnDir1 : kSgnDir0;
@@ -363,6 +408,7 @@ struct Walker {
   }
 
   __device__ __forceinline__ Dd2 result() const {
+    if (MODE == kSep) return kSmemAcc ? *accs : Dd2{arh, arl, aih, ail};
     if (kSmemAcc) {
       const Dd2 a = *accs;
       if (PLAIN) return Dd2{a.re_hi, 0.0, a.im_hi, 0.0};
@@ -383,18 +429,18 @@ struct Walker {
 // in a separate ptxas allocation unit is what lets ptxas hold the half-walk loop counter in
 // a uniform register and feed the column operands from LDCU; inlined into the leaf loop
 // (a loop nest with the build's loop) it fell back to per-thread LDC and spilled.
-template <int N, int ALG, bool PLAIN, bool SA, class Cols>
+template <int N, int ALG, int MODE, bool SA, class Cols>
 __device__ __noinline__ Dd2 chunk_fast(const Cols cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
-  Walker<N, ALG, PLAIN, SA> w;
+  Walker<N, ALG, MODE, SA> w;
   w.zero_acc();
   w.fast_chunk(cols, at, q, c, zero);
   return w.result();
 }
 
 // Ragged piece [ga, gb) of one chunk (range ends, tiny n).
-template <int N, int ALG, bool PLAIN, bool SA>
+template <int N, int ALG, int MODE, bool SA>
 __device__ __noinline__ Dd2 chunk_generic(const double2* __restrict__ at, uint64_t ga, uint64_t gb) {
-  Walker<N, ALG, PLAIN, SA> w;
+  Walker<N, ALG, MODE, SA> w;
   w.zero_acc();
   w.generic_walk(at, ga, gb);
   return w.result();
@@ -416,7 +462,7 @@ __device__ __forceinline__ void leaf_chunk_window(uint64_t leaf_id, int c, int l
 // One leaf = 2^lam consecutive chunks walked in order by one thread; chunk partials are
 // combined in order with double-double additions.  kFast: every chunk lies inside the
 // range and c >= 5 (decided by the caller from block-uniform values).
-template <int N, int ALG, bool kFast, bool PLAIN, class Cols>
+template <int N, int ALG, bool kFast, int MODE, class Cols>
 __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
                                          int c, int lam, uint64_t lo, uint64_t hi, int zero) {
   // shared-memory chunk accumulator only in the sweep kernel (ConstColumns; its smem layout
@@ -430,12 +476,12 @@ __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __rest
   for (uint64_t k = k0; k < k1; ++k) {
     const uint64_t q = (leaf_id << lam) + k;
     if (kFast) {
-      acc = part_add<PLAIN>(acc, chunk_fast<N, ALG, PLAIN, SA>(cols, at, q, c, zero));
+      acc = part_add<MODE>(acc, chunk_fast<N, ALG, MODE, SA>(cols, at, q, c, zero));
     } else {
       const uint64_t g0 = q << c, g1 = g0 + (1ull << c);
       const uint64_t ga = g0 > lo ? g0 : lo;
       const uint64_t gb = g1 < hi ? g1 : hi;
-      if (ga < gb) acc = part_add<PLAIN>(acc, chunk_generic<N, ALG, PLAIN, SA>(at, ga, gb));
+      if (ga < gb) acc = part_add<MODE>(acc, chunk_generic<N, ALG, MODE, SA>(at, ga, gb));
     }
   }
   return acc;
@@ -456,13 +502,13 @@ __device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, 
 
 // Canonical block reduction: contiguous pairwise tree over the block's threads (leaves),
 // node = left + right in double-double.  Result valid in red[0].
-template <bool PLAIN = false>
+template <int MODE = kComp>
 __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
   const int tid = threadIdx.x, nt = blockDim.x;
   red[tid] = mine;
   __syncthreads();
   for (int o = 1; o < nt; o <<= 1) {
-    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = part_add<PLAIN>(red[tid], red[tid + o]);
+    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = part_add<MODE>(red[tid], red[tid + o]);
     __syncthreads();
   }
 }
@@ -470,7 +516,7 @@ __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
 // ------------------------------------------------------------------ kernels
 // One block = one unit of the canonical plan.  Dynamic shared memory: N*N double2
 // (transposed matrix) + blockDim Dd2 (reduction).
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
   // [N*N: at][blockDim Dd2: tree][blockDim Dd2: chunk accumulators (Walker)]
@@ -485,10 +531,10 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) 
   const int ubits = args.block_bits + args.lam + args.c;          // log2(unit terms)
   const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
   Dd2 mine;
-  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
 
-  block_tree<PLAIN>(red, mine);
+  block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
 }
 
@@ -519,7 +565,7 @@ __device__ __forceinline__ void build_tab(const double2* at, double2* tab, int c
 // kernel's (same table values, same flips, same accumulation), i.e. bit-identical results.
 constexpr int kSmallLog2 = 21;
 
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs args) {
   extern __shared__ double2 smem[];
   // [N*N: at][kTabRows*N: tab][blockDim Dd2: tree]  (register chunk accumulators)
@@ -536,9 +582,9 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs 
   const int ubits = args.block_bits + args.lam + args.c;
   const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
   Dd2 mine;
-  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  block_tree<PLAIN>(red, mine);
+  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
 }
 
@@ -550,10 +596,31 @@ struct FinishArgs {
   double2* out;
   Dd2* out_dd;
   int do_scale, scale_exp, scale_dd;
+  int sep;      // 0; or kSep partials: +1 / -1 = sign of (even - odd) (Ryser, odd n: -1)
 };
 
 __device__ __forceinline__ void finish_root(const Dd2& r, const FinishArgs& f) {
   const int e = f.do_scale ? f.scale_exp : 0;
+  if (f.sep) {
+    // separate addition: the ONE subtraction of the odd-index sum from the even-index sum
+    // ("(0+2+4+6)-(1+3+5+7)"), then the exact sign and power-of-two factors
+    if (f.out_dd) {
+      Dd2 o = r;
+      if (f.scale_dd) {
+        o.re_hi = ldexp(o.re_hi, e); o.re_lo = ldexp(o.re_lo, e);
+        o.im_hi = ldexp(o.im_hi, e); o.im_lo = ldexp(o.im_lo, e);
+      }
+      *f.out_dd = o;
+    }
+    if (f.out) {
+      double re = ldexp(__dsub_rn(r.re_hi, r.re_lo), e) * (double)f.sep;
+      double im = ldexp(__dsub_rn(r.im_hi, r.im_lo), e) * (double)f.sep;
+      if (re == 0.0) re = 0.0;
+      if (im == 0.0) im = 0.0;
+      *f.out = make_double2(re, im);
+    }
+    return;
+  }
   if (f.out_dd) {
     Dd2 o = r;
     if (f.scale_dd) {            // exact power-of-two scaling of both halves
@@ -578,7 +645,7 @@ __device__ __forceinline__ void finish_root(const Dd2& r, const FinishArgs& f) {
 // canonical tree (units <= blockDim, a power of two: block_tree over blockDim entries with
 // zero padding pairs them exactly as combine_kernel does) and finishes.  Same bits as sweep +
 // combine, one launch fewer (M1: the combine launch measured ~5 us of a ~20 us call).
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const SweepArgs args, const FinishArgs fin) {
   extern __shared__ double2 smem[];
   double2* at = smem;
@@ -592,14 +659,14 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 mine;
-  if (args.c >= 5) mine = walk_leaf<N, ALG, true, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  else mine = walk_leaf<N, ALG, false, PLAIN>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
-  block_tree<PLAIN>(red, mine);
+  if (args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
   cooperative_groups::this_grid().sync();
   if (blockIdx.x == 0) {
     const Dd2 v = threadIdx.x < gridDim.x ? args.unit_out[threadIdx.x] : Dd2{0.0, 0.0, 0.0, 0.0};
-    block_tree<PLAIN>(red, v);
+    block_tree<MODE>(red, v);
     if (threadIdx.x == 0) finish_root(red[0], fin);
   }
 }
@@ -648,7 +715,9 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
       double im = __dadd_rn(ldexp(r.im_hi, args.scale_exp), ldexp(r.im_lo, args.scale_exp));
       if (re == 0.0) re = 0.0;   // canonical +0
       if (im == 0.0) im = 0.0;
-      args.out[b] = make_double2(re, im);
+      if (args.out) args.out[b] = make_double2(re, im);
+      // P(S|T) ~ |Perm(U_ST)|^2: one fused multiply-add of the rounded components
+      if (args.out_abs2) args.out_abs2[b] = __fma_rn(re, re, __dmul_rn(im, im));
     }
   }
 }
@@ -676,7 +745,7 @@ static __global__ void stage_columns_kernel(const double2* __restrict__ A, int n
 using SweepLauncher = cudaError_t (*)(const SweepArgs&, int64_t units, double2* staging, cudaStream_t);
 using BatchedLauncher = cudaError_t (*)(const BatchedArgs&, int grid, cudaStream_t);
 
-template <int N, int ALG, bool PLAIN = false>
+template <int N, int ALG, int MODE = kComp>
 cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cudaStream_t st) {
   const int c_tab = a.c < kCMax ? a.c : kCMax;
   const int col0 = (ALG == kGlynn) ? 1 : 0;
@@ -691,31 +760,31 @@ cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cu
   const int threads = 1 << a.block_bits;
   const size_t smem = sizeof(double2) * N * N + 2 * sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep_kernel<N, ALG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  sweep_kernel<N, ALG, PLAIN><<<(unsigned)units, threads, smem, st>>>(a);
+  sweep_kernel<N, ALG, MODE><<<(unsigned)units, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, int MODE>
 cudaError_t launch_sweep_small(const SweepArgs& a, int64_t units, double2*, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
   const size_t smem = sizeof(double2) * (N * N + kTabRows * N) + sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_small_kernel<N, ALG, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(sweep_small_kernel<N, ALG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  sweep_small_kernel<N, ALG, PLAIN><<<(unsigned)units, threads, smem, st>>>(a);
+  sweep_small_kernel<N, ALG, MODE><<<(unsigned)units, threads, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-template <int N, int ALG, bool PLAIN>
+template <int N, int ALG, int MODE>
 cudaError_t launch_sweep_small_fused(const SweepArgs& a, const FinishArgs& f, int64_t units, cudaStream_t st) {
   const int threads = 1 << a.block_bits;
   const size_t smem = sizeof(double2) * (N * N + kTabRows * N) + sizeof(Dd2) * threads;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_small_fused_kernel<N, ALG, PLAIN>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_small_fused_kernel<N, ALG, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -729,7 +798,7 @@ cudaError_t launch_sweep_small_fused(const SweepArgs& a, const FinishArgs& f, in
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, sweep_small_fused_kernel<N, ALG, PLAIN>, a, f);
+  return cudaLaunchKernelEx(&cfg, sweep_small_fused_kernel<N, ALG, MODE>, a, f);
 }
 
 template <int N>
@@ -751,20 +820,24 @@ cudaError_t launch_batched(const BatchedArgs& a, int grid, cudaStream_t st) {
 namespace permb200 {
 template <int ALG, int LO, int... Is>
 void fill_sweep(SweepLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, false>), ...);
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, kComp>), ...);
 }
 template <int ALG, int LO, int... Is>
 void fill_sweep_plain(SweepLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, true>), ...);
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, kPlain>), ...);
 }
-template <int ALG, bool PLAIN, int LO, int... Is>
+template <int ALG, int LO, int... Is>
+void fill_sweep_sep(SweepLauncher* table, std::integer_sequence<int, Is...>) {
+  ((table[LO + Is] = &launch_sweep<LO + Is, ALG, kSep>), ...);
+}
+template <int ALG, int MODE, int LO, int... Is>
 void fill_sweep_small(SweepLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_sweep_small<LO + Is, ALG, PLAIN>), ...);
+  ((table[LO + Is] = &launch_sweep_small<LO + Is, ALG, MODE>), ...);
 }
 using FusedLauncher = cudaError_t (*)(const SweepArgs&, const FinishArgs&, int64_t units, cudaStream_t);
-template <int ALG, bool PLAIN, int LO, int... Is>
+template <int ALG, int MODE, int LO, int... Is>
 void fill_sweep_small_fused(FusedLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_sweep_small_fused<LO + Is, ALG, PLAIN>), ...);
+  ((table[LO + Is] = &launch_sweep_small_fused<LO + Is, ALG, MODE>), ...);
 }
 template <int LO, int... Is>
 void fill_batched(BatchedLauncher* table, std::integer_sequence<int, Is...>) {

@@ -23,6 +23,10 @@ void register_dd_glynn_a(SweepLauncher* t);
 void register_dd_glynn_b(SweepLauncher* t);
 void register_dd_ryser_a(SweepLauncher* t);
 void register_dd_ryser_b(SweepLauncher* t);
+void register_sep_glynn_a(SweepLauncher* t);
+void register_sep_glynn_b(SweepLauncher* t);
+void register_sep_ryser_a(SweepLauncher* t);
+void register_sep_ryser_b(SweepLauncher* t);
 void register_small(SweepLauncher (*t)[kNMax + 1]);
 void register_small_fused(FusedLauncher (*t)[kNMax + 1]);
 void register_batched_a(BatchedLauncher* t);

@@ -9,7 +9,9 @@ all_reduce(SUM) of a (world, 4) float64 buffer in which rank r fills only row r 
 slot has exactly one non-zero contributor, so the sum is exact and order-independent (an
 all-gather expressed as the single NCCL all-reduce the north_star names).  Every rank then
 combines the roots with the same pairwise tree, so for world | units (powers of two) the
-result is bit-identical to the single-GPU perm_glynn / perm_ryser.
+result is bit-identical to the single-GPU perm_glynn / perm_ryser.  Other world sizes (3, 5,
+6, 7 GPUs) gather the whole unit-partial table instead (reduce_partials): still one
+collective, still bit-identical.
 """
 from __future__ import annotations
 
@@ -33,29 +35,59 @@ def gather_roots(local_root: torch.Tensor, world: int, rank: int, group=None) ->
     return buf
 
 
+def subtree_aligned(units: int, world: int) -> bool:
+    """True when every rank's contiguous unit block is one subtree of the canonical tree
+    (world a power of two dividing `units`): then one root per rank suffices."""
+    return world & (world - 1) == 0 and units % world == 0
+
+
+def reduce_partials(parts: torch.Tensor, n: int, alg: int, units: int, ulo: int, uhi: int, world: int, rank: int,
+                    group=None, combine: Optional[Callable] = None) -> torch.Tensor:
+    """This rank's unit partials [ulo, uhi) -> the scaled permanent on every rank, with ONE
+    collective and bit-identical to the single-GPU combine for ANY world size:
+
+      world == 1        combine(parts) directly (no collective);
+      subtree-aligned   each rank reduces its block to its subtree root, one all_reduce(SUM) of a
+                        (world, 4) one-hot table gathers the roots exactly, combine(roots);
+      otherwise         (3, 5, 6, 7 ... GPUs: blocks are not subtrees) one all_reduce(SUM) of the
+                        (units, 4) table, each unit with exactly one non-zero contributor
+                        (exact), then combine over all units -- units x 32 B (4 MiB at n = 40)."""
+    import paper_1606_05836_b200 as pb
+    combine = combine or pb.combine
+    if world == 1:
+        return combine(parts, n, alg, scale=True)[0]
+    dev = parts.device
+    if subtree_aligned(units, world):
+        if uhi > ulo:
+            root = combine(parts, n, alg, scale=False)[1]
+        else:
+            root = torch.zeros(4, dtype=torch.float64, device=dev)
+        return combine(gather_roots(root, world, rank, group), n, alg, scale=True)[0]
+    table = torch.zeros((units, 4), dtype=torch.float64, device=dev)
+    if uhi > ulo:
+        table[ulo:uhi] = parts
+    dist.all_reduce(table, op=dist.ReduceOp.SUM, group=group)
+    return combine(table, n, alg, scale=True)[0]
+
+
 def perm_dist(A: torch.Tensor, alg: str = "glynn", group=None,
               sweep: Optional[Callable] = None, combine: Optional[Callable] = None) -> torch.Tensor:
     """Perm(A) with the Gray-index range split over the ranks of `group` (default: WORLD).
 
     A must be the same n x n complex128 matrix on every rank (on that rank's GPU).  Returns
-    the 0-d complex128 result on every rank.  `sweep` / `combine` default to the CUDA
+    the 0-d complex128 result on every rank, bit-identical to the single-GPU perm_glynn /
+    perm_ryser for any world size (reduce_partials).  `sweep` / `combine` default to the CUDA
     kernels (paper_1606_05836_b200.sweep_units / combine)."""
     import paper_1606_05836_b200 as pb
     sweep = sweep or pb.sweep_units
-    combine = combine or pb.combine
     n = A.shape[0]
     a = pb._alg(alg)
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     P = pb.plan(n, a)
     ulo, uhi = unit_range(P.units, world, rank)
-    if uhi > ulo:
-        root = combine(sweep(A, a, ulo, uhi), n, a, scale=False)[1]
-    else:
-        root = torch.zeros(4, dtype=torch.float64, device=A.device)
-    roots = gather_roots(root, world, rank, group)
-    val, _ = combine(roots, n, a, scale=True)
-    return val
+    parts = sweep(A, a, ulo, uhi) if uhi > ulo else torch.zeros((0, 4), dtype=torch.float64, device=A.device)
+    return reduce_partials(parts, n, a, P.units, ulo, uhi, world, rank, group, combine)
 
 
 def batch_range(batch: int, world: int, rank: int) -> tuple[int, int]:

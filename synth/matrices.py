@@ -26,6 +26,7 @@ __all__ = [
     "eye", "bernoulli", "diag_1pi", "all_r", "rank1_factors", "block_diag", "menage",
     "x_eye_plus_ones", "random_int", "random_complex_small", "sha256", "workload",
     "WORKLOADS",
+    "permutation",
 ]
 
 
@@ -132,6 +133,12 @@ def random_complex_small(n: int, seed: int) -> np.ndarray:
     """Entries uniform in [-1,1]^2 (SPEC.md:159 oracle-equivalence recipe)."""
     rng = np.random.default_rng(seed)
     return _c128(rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n)))
+
+
+def permutation(count: int, seed: int) -> np.ndarray:
+    """Seeded random permutation of [0, count) (int64): the "random order" of the summation-
+    order experiments (Table AV) is an input, drawn here."""
+    return np.random.default_rng(seed).permutation(count).astype(np.int64)
 
 
 def sha256(a: np.ndarray) -> str:

@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "permb200.h")
 
 def _declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(perm_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(perm_\w+)\s*\(", text, re.M)))
 
 
 def test_library_loads_and_exports_every_declared_symbol():
@@ -44,9 +44,15 @@ def test_invalid_arguments_rejected_without_cuda():
     assert L.perm_glynn_batched(None, 4, 0, None, None) == _lib.PERM_OK     # empty batch: no-op
     assert L.perm_glynn_range(buf, 4, 5, 4, buf, None) == _lib.PERM_EINVAL   # lo > hi
     assert L.perm_glynn_range(buf, 4, 0, 9, buf, None) == _lib.PERM_EINVAL   # hi > 2^(n-1)
-    assert L.perm_sweep_units(buf, 4, 6, 0, 1, buf, None) == _lib.PERM_EINVAL  # bad alg
+    assert L.perm_sweep_units(buf, 4, 8, 0, 1, buf, None) == _lib.PERM_EINVAL  # bad alg
+    assert L.perm_sweep_units(buf, 41, _lib.ALG_GLYNN_SEP, 0, 1, buf, None) == _lib.PERM_EINVAL  # sep: n <= 40
+    assert L.perm_glynn_batched_abs2(buf, 4, 3, None, None) == _lib.PERM_EINVAL   # null out
+    assert L.perm_glynn_batched_abs2(None, 4, 0, None, None) == _lib.PERM_OK      # empty batch
+    assert L.perm_sum_ordered(buf, 0, buf, 4, 0, buf, None) == _lib.PERM_EINVAL   # count < 1
+    assert L.perm_sum_ordered(buf, 4, None, 4, 0, buf, None) == _lib.PERM_EINVAL  # null order
+    assert L.perm_launch_count() == 0                                             # nothing launched
     assert L.perm_sweep_units(buf, 4, -1, 0, 1, buf, None) == _lib.PERM_EINVAL
-    assert L.perm_range(buf, 4, 6, 0, 1, buf, None) == _lib.PERM_EINVAL
+    assert L.perm_range(buf, 4, 8, 0, 1, buf, None) == _lib.PERM_EINVAL
     assert L.perm_range(buf, 4, pb.ALG_RYSER_PLAIN, 0, 17, buf, None) == _lib.PERM_EINVAL
     assert L.perm_range(buf, 4, pb.ALG_RYSER_DD, 0, 17, buf, None) == _lib.PERM_EINVAL   # hi > 2^n
     assert L.perm_glynn_dd(None, 4, buf, None) == _lib.PERM_EINVAL

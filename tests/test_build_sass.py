@@ -56,7 +56,7 @@ def test_hot_loop_has_no_spills_up_to_n51(obj, n, alg):
     import sys
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from sass_loop_stats import loop_stats
-    name, length, c = loop_stats(_sass(obj), f"sweep_kernelILi{n}ELi{alg}ELb0")
+    name, length, c = loop_stats(_sass(obj), f"sweep_kernelILi{n}ELi{alg}ELi0E")
     assert length > 0
     spills = sum(v for k, v in c.items() if k.startswith(("STL", "LDL")))
     assert spills == 0, (n, spills)

@@ -11,7 +11,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1606_05836_b200.dist import gather_roots, unit_range
+from paper_1606_05836_b200.dist import gather_roots, subtree_aligned, unit_range
+from standins import oracle_sweep, tree_combine
 
 
 def _free_port():
@@ -114,3 +115,46 @@ def test_gloo_batched_sharding_one_all_gather():
     for _, out in res:
         assert out.shape == (7,)
         assert np.array_equal(out, want)
+
+
+def _perm_dist_worker(rank, world, port, n, alg, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import synth
+    from paper_1606_05836_b200.dist import perm_dist
+    A = torch.from_numpy(synth.gaussian(n, 99))
+    v = perm_dist(A, alg, sweep=oracle_sweep, combine=tree_combine)
+    out_q.put((rank, complex(v.item())))
+    dist.destroy_process_group()
+
+
+def _run_world(world, n, alg):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_perm_dist_worker, args=(r, world, port, n, alg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return [v for _, v in res]
+
+
+@pytest.mark.parametrize("alg", ["glynn", "ryser"])
+def test_perm_dist_any_world_size_is_bit_identical(alg):
+    """perm_dist on 2 ranks (subtree-aligned: one root per rank) and 3 ranks (not aligned: the
+    whole unit table in one all_reduce) equals the single-process canonical combine bit for
+    bit (world sizes that are not powers of two)."""
+    import synth
+    import paper_1606_05836_b200 as pb
+    n = 14
+    A = torch.from_numpy(synth.gaussian(n, 99))
+    P = pb.plan(n, pb._alg(alg))
+    one = complex(tree_combine(oracle_sweep(A, pb._alg(alg), 0, P.units), n, pb._alg(alg))[0].item())
+    assert subtree_aligned(P.units, 2) and not subtree_aligned(P.units, 3)
+    for world in (2, 3):
+        vals = _run_world(world, n, alg)
+        assert all(v == one for v in vals), (world, vals, one)

@@ -13,6 +13,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from standins import oracle_sweep, tree_combine
+
 N = 20
 SEG = 16
 
@@ -23,30 +25,6 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
-
-
-def oracle_sweep(A, alg, lo, hi):
-    import oracle
-    import paper_1606_05836_b200 as pb
-    a = A.numpy()
-    P = pb.plan(a.shape[0], alg)
-    out = [oracle.glynn_partial(a, u * P.unit_terms, (u + 1) * P.unit_terms, threads=1)[0].as4() for u in range(lo, hi)]
-    return torch.from_numpy(np.stack(out))
-
-
-def tree_combine(parts, n, alg, scale=True):
-    """Canonical tree (left + right, zero padding to a power of two) with the oracle's dd add."""
-    import oracle
-    v = [oracle.DD.from4(r) for r in parts.numpy()]
-    size = 1
-    while size < len(v):
-        size *= 2
-    v += [oracle.DD(0.0, 0.0, 0.0, 0.0)] * (size - len(v))
-    while len(v) > 1:
-        v = [v[i] + v[i + 1] for i in range(0, len(v), 2)]
-    root = v[0]
-    val = root.scaled(-(n - 1)).to_complex() if scale else None
-    return torch.tensor(val, dtype=torch.complex128), torch.from_numpy(root.as4())
 
 
 def _worker(rank, world, port, prefix, max_segments, out_q, use_store=False, tag=""):
