@@ -318,7 +318,7 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   a.slot = slot;
   a.col_base = slot * kTabRows * kNMax;
   CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "sweep launch");
-  note_launch(a.c >= 5 ? 2 : 1);         // column staging (c >= 5) + sweep
+  note_launch(a.c >= kMinFastC ? 2 : 1);   // column staging (fast path) + sweep
   CUDA_TRY(cudaEventRecord(ds.ev[slot], st), "cudaEventRecord");
   ds.used[slot] = true;
   return PERM_OK;
@@ -339,7 +339,7 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
   const uint64_t T = 1ULL << P.log2_terms;
   int rc;
   init_tables();
-  if (!is_dd(alg) && P.log2_terms <= kSmallLog2 && g_small_fused[alg][n] && P.units <= (1LL << P.block_bits)) {
+  if (!is_dd(alg) && P.log2_terms <= kSmallLog2 && g_small_fused[alg][n] && P.units <= (8LL << P.block_bits)) {
     // small n: sweep + combine in one cooperative launch (same bits as the two-kernel path)
     SweepArgs a;
     a.A = reinterpret_cast<const double2*>(A);
@@ -463,7 +463,7 @@ int perm_sweep_units_custom(const perm_c128* A, int n, int alg, int chunk_bits, 
   perm_plan_t P;
   make_plan(n, alg, &P);
   const int wmax = is_dd(alg) ? 6 : 7;
-  if (chunk_bits < 5 || chunk_bits > kCMax || leaf_bits < 0 || block_bits < 0 || block_bits > wmax ||
+  if (chunk_bits < kMinFastC || chunk_bits > kCMax || leaf_bits < 0 || block_bits < 0 || block_bits > wmax ||
       chunk_bits + leaf_bits + block_bits > P.log2_terms || P.log2_terms - chunk_bits - leaf_bits - block_bits > 40)
     return PERM_EINVAL;
   P.chunk_bits = chunk_bits; P.leaf_bits = leaf_bits; P.block_bits = block_bits;

@@ -44,6 +44,7 @@ enum { kComp = 0, kPlain = 1, kSep = 2 };
 
 constexpr int kNMax = 64;      // largest n
 constexpr int kCMax = 12;      // largest chunk_bits
+constexpr int kMinFastC = 3;   // smallest chunk_bits of the uniform-column fast path (half-walks of >= 4 steps)
 constexpr int kTabBits = 16;   // Gray bits covered by a column table (rows for bits >= c are zero)
 constexpr int kTabRows = 2 * kTabBits;   // row 2b+d = signed step vector of bit b, direction d
 constexpr int kSlots = 1;      // constant-memory column slots per translation unit (32 KB each)
@@ -363,7 +364,7 @@ struct Walker {
     else acc_add(mr, mi);
   }
 
-  // Full aligned chunk q (Gray indices [q 2^c, (q+1) 2^c)), c >= 5.
+  // Full aligned chunk q (Gray indices [q 2^c, (q+1) 2^c)), c >= kMinFastC.
   template <class Cols>
   __device__ __forceinline__ void fast_chunk(const Cols& cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
     const uint64_t g0 = q << c;
@@ -425,7 +426,7 @@ struct Walker {
   }
 };
 
-// One full aligned chunk q, c >= 5, as its own (non-inlined) function.  Keeping the walk
+// One full aligned chunk q, c >= kMinFastC, as its own (non-inlined) function.  Keeping the walk
 // in a separate ptxas allocation unit is what lets ptxas hold the half-walk loop counter in
 // a uniform register and feed the column operands from LDCU; inlined into the leaf loop
 // (a loop nest with the build's loop) it fell back to per-thread LDC and spilled.
@@ -461,7 +462,7 @@ __device__ __forceinline__ void leaf_chunk_window(uint64_t leaf_id, int c, int l
 
 // One leaf = 2^lam consecutive chunks walked in order by one thread; chunk partials are
 // combined in order with double-double additions.  kFast: every chunk lies inside the
-// range and c >= 5 (decided by the caller from block-uniform values).
+// range and c >= kMinFastC (decided by the caller from block-uniform values).
 template <int N, int ALG, bool kFast, int MODE, class Cols>
 __device__ __forceinline__ Dd2 walk_leaf(const Cols& cols, const double2* __restrict__ at, uint64_t leaf_id,
                                          int c, int lam, uint64_t lo, uint64_t hi, int zero) {
@@ -531,7 +532,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_kernel(const SweepArgs args) 
   const int ubits = args.block_bits + args.lam + args.c;          // log2(unit terms)
   const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
   Dd2 mine;
-  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  if (inside && args.c >= kMinFastC) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
 
   block_tree<MODE>(red, mine);
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs 
   const int ubits = args.block_bits + args.lam + args.c;
   const bool inside = (unit << ubits) >= args.lo && ((unit + 1) << ubits) <= args.hi;
   Dd2 mine;
-  if (inside && args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  if (inside && args.c >= kMinFastC) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
@@ -659,13 +660,26 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 mine;
-  if (args.c >= 5) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  if (args.c >= kMinFastC) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
   cooperative_groups::this_grid().sync();
   if (blockIdx.x == 0) {
-    const Dd2 v = threadIdx.x < gridDim.x ? args.unit_out[threadIdx.x] : Dd2{0.0, 0.0, 0.0, 0.0};
+    // units (a power of two) <= 8 * blockDim: thread t first reduces the aligned segment
+    // [t S, (t+1) S) (the bottom levels of the canonical tree), then the block tree
+    const int S = gridDim.x > blockDim.x ? (int)(gridDim.x / blockDim.x) : 1;
+    Dd2 stack[4];
+    int top = 0;
+    for (int k = 0; k < S; ++k) {
+      const unsigned idx = threadIdx.x * S + k;
+      Dd2 v = idx < gridDim.x ? args.unit_out[idx] : Dd2{0.0, 0.0, 0.0, 0.0};
+      int lvl = 0;
+      for (int kk = k; kk & 1; kk >>= 1) { v = part_add<MODE>(stack[lvl], v); ++lvl; }
+      stack[lvl] = v;
+      if (lvl > top) top = lvl;
+    }
+    const Dd2 v = stack[top];
     block_tree<MODE>(red, v);
     if (threadIdx.x == 0) finish_root(red[0], fin);
   }
@@ -706,7 +720,7 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
     const SmemColumns<N> cols{tab};
     const uint64_t terms = 1ull << (N - 1);
     Dd2 mine;
-    if (args.c >= 5) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
+    if (args.c >= kMinFastC) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
     else mine = walk_leaf<N, kGlynn, false, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
     block_tree(red, mine);
     if (threadIdx.x == 0) {
@@ -749,7 +763,7 @@ template <int N, int ALG, int MODE = kComp>
 cudaError_t launch_sweep(const SweepArgs& a, int64_t units, double2* staging, cudaStream_t st) {
   const int c_tab = a.c < kCMax ? a.c : kCMax;
   const int col0 = (ALG == kGlynn) ? 1 : 0;
-  if (a.c >= 5) {
+  if (a.c >= kMinFastC) {
     stage_columns_kernel<<<1, 256, 0, st>>>(a.A, N, col0, c_tab, (ALG == kGlynn) ? 2.0 : 1.0, staging);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -180,3 +180,34 @@ def test_launch_count_matches_the_path():
     k0 = pb.launch_count()
     pb.glynn_batched(T(np.stack([synth.gaussian(8, s) for s in range(5)])))
     assert pb.launch_count() - k0 == 1
+
+
+# ----------------------------------------------------------------- Table AV rows (Ryser on J_N)
+@pytest.mark.parametrize("N", [8, 13, 14, 17, 20])
+def test_table_av_J_N_all_orders_vs_oracle(N):
+    """The four summation orders of Table AV on Ryser J_N against the exact N!
+    (oracle.exact / int128 up to its range, else the oracle's dd walk): exact while every term
+    and partial sum stays an integer below 2^53 (N <= 13), within the walk-aware bound plus the
+    order's accumulation allowance beyond."""
+    A = synth.ones(N)
+    dA = T(A)
+    P = pb.plan(N, pb.ALG_RYSER)
+    part = oracle.partial_ex(A, 0, P.terms, "ryser")
+    ref = float(math.factorial(N))
+    assert abs(part.dd.to_complex() - ref) <= 1e-20 * ref        # the oracle walk itself: exact here
+    parts, count = _chunk_partials(dA, "ryser_plain", N)
+    rows = {
+        "original": cval(pb.sum_ordered(parts, torch.arange(count, dtype=torch.int64, device=DEV), N, "ryser_plain")),
+        "random": cval(pb.sum_ordered(parts, torch.from_numpy(synth.permutation(count, 977 + N)).to(DEV), N,
+                                      "ryser_plain")),
+        "merge": cval(pb.combine(parts, N, "ryser_plain")[0]),
+        "separate": cval(pb.perm_alg(dA, "ryser_sep")),
+    }
+    Ps = pb.plan(N, pb.ALG_RYSER_SEP)
+    for name, got in rows.items():
+        if N <= 13:
+            assert got == ref, (name, got)
+            continue
+        extra = U * (count + 48) * part.l1 if name != "separate" else 2 * plain_extra(part, Ps) + U * ref
+        c = 5 if name != "separate" else Ps.chunk_bits
+        check_B(got, part, N, c, ref=complex(ref), extra=extra, what=f"J_{N} {name}")
