@@ -7,3 +7,4 @@ timeout 600 python tools/r02/batched_run.py --out $O/batched.json > $O/batched.l
 timeout 600 python bench.py > $O/bench_n1.json 2> $O/bench_n1.err; echo "bench rc=$?" >> $O/status.txt
 PERMB200_DIST_BACKEND=gloo timeout 600 python bench.py --gpus 2 --steps 2 --warmup 3 > $O/bench_gloo2.json 2> $O/bench_gloo2.err; echo "bench2 rc=$?" >> $O/status.txt
 timeout 900 python tools/r02/table_av.py --out $O/r02_precision > $O/table_av.log 2>&1; echo "tableav rc=$?" >> $O/status.txt
+for v in 00 10 01 11 00 10 01 11; do echo "variant $v" >> $O/sweep_variants.log; timeout 120 tools/microbench/sweep_bench_$v 8 >> $O/sweep_variants.log 2>&1; done
