@@ -775,7 +775,11 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
 // blocks/SM, 9.2 waves for M2's 4096 permanents; ncu profiles/r01_batched_m2_*) leaves warps
 // idle.  At 4 blocks (<= 128 registers) chunk_fast<16> still has no spills (only the kernel
 // body spills a few values across the chunk call).
+#ifdef PERMB200_BATCHED_MINB          // A/B experiments (tools/microbench/batched_bench.cu)
+__host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? PERMB200_BATCHED_MINB : N <= 20 ? 3 : 1; }
+#else
 __host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? 4 : N <= 20 ? 3 : 1; }
+#endif
 
 template <int N>
 __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kernel(const BatchedArgs args) {
