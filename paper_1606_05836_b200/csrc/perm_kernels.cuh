@@ -44,22 +44,15 @@ enum { kComp = 0, kPlain = 1, kSep = 2 };
 
 constexpr int kNMax = 64;      // largest n
 constexpr int kCMax = 12;      // largest chunk_bits
-constexpr int kMinFastC = 3;   // smallest chunk_bits of the uniform-column fast path (half-walks of >= 4 steps)
+// Smallest chunk_bits of the uniform-column fast path: half_walk takes the direction of the bit-1
+// flip from bit 2 of its local step, which equals bit 2 of the chunk index only when the second
+// half starts at a multiple of 8, i.e. c >= 4 (c = 3 measured wrong results, r02 M1 plan sweep).
+constexpr int kMinFastC = 4;
 constexpr int kTabBits = 16;   // Gray bits covered by a column table (rows for bits >= c are zero)
 constexpr int kTabRows = 2 * kTabBits;   // row 2b+d = signed step vector of bit b, direction d
 constexpr int kSlots = 1;      // constant-memory column slots per translation unit (32 KB each)
 constexpr int kMaxBlock = 128; // threads per block (block_bits <= 7)
 
-// Code-shape switch of the half-walk's bit-1 flip (Walker::half_walk): 1 = static table row with
-// a uniform sign XOR, 0 = the direction-selected (dynamic) row.  Bit-identical results; A/B
-// timing with tools/microbench/sweep_bench.cu.
-#ifndef PERMB200_R2_XORSIGN
-#define PERMB200_R2_XORSIGN 0
-#endif
-// 1 = the half-walk loop rotated by one step (Walker::half_walk_rot), 0 = half_walk.
-#ifndef PERMB200_R0_ROTATE
-#define PERMB200_R0_ROTATE 0
-#endif
 
 struct Dd2 { double re_hi, re_lo, im_hi, im_lo; };
 
@@ -323,21 +316,6 @@ struct Walker {
     }
   }
 
-  // s_i <- s_i + (neg ? -1 : +1) * table[row]_i with a warp-uniform `neg`: the sign bit of the
-  // uniform operand is flipped (an integer XOR, exact) and the update stays one DADD.
-  template <class Cols>
-  __device__ __forceinline__ void flip_xorsign(const Cols& cols, int row, bool neg) {
-    const unsigned mask = neg ? 0x80000000u : 0u;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double2 v = cols.get(row, i);
-      const double vx = __hiloint2double(__double2hiint(v.x) ^ mask, __double2loint(v.x));
-      const double vy = __hiloint2double(__double2hiint(v.y) ^ mask, __double2loint(v.y));
-      s[i].x = __dadd_rn(s[i].x, vx);
-      s[i].y = __dadd_rn(s[i].y, vy);
-    }
-  }
-
   // s_i <- s_i + sg * table[row]_i with a per-thread sign sg = +-1 (the one mid-chunk flip).
   template <class Cols>
   __device__ __forceinline__ void flip_signed(const Cols& cols, int row, double sg) {
@@ -372,14 +350,7 @@ struct Walker {
         const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
         const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
         const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
-        if (r == 2 && PERMB200_R2_XORSIGN) {
-          // bit 1's direction alternates between iterations: a STATIC table row (+u_1) with a
-          // warp-uniform sign operand, s + (+-1) u rounded once (= the signed row's DADD), so
-          // the column loads have compile-time addresses and ptxas can issue them early
-          flip_xorsign(cols, plus_row(1) + tz, (d ? kSgnDir1 : kSgnDir0) < 0.0);
-        } else {
-          flip_row(cols, row);
-        }
+        flip_row(cols, row);
         const double2 p = row_product<N>(s);
         if (MODE == kSep) {          // parity of g = parity of r (T0 and t + 4 are multiples of 4)
           if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
@@ -391,51 +362,6 @@ struct Walker {
         if (MODE == kSep) { acc_add_sep(mr, mi, orr, oi); orr = 0.0; oi = 0.0; }
         else acc_add(mr, mi);
         mr = 0.0; mi = 0.0;
-      }
-    }
-    if (MODE == kSep) acc_add_sep(mr, mi, orr, oi);
-    else acc_add(mr, mi);
-  }
-
-  // Signed accumulation of the term of unrolled step r (parity of g = parity of r).
-  __device__ __forceinline__ void accum(const double2& p, int r, double& mr, double& mi, double& orr, double& oi) {
-    if (MODE == kSep) {
-      if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
-      else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
-    } else if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
-    else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
-  }
-
-  // The same half-walk with the loop ROTATED by one step: a loop trip runs steps r = 1, 2, 3
-  // of iteration t and then the r = 0 step of iteration t + 4, so the dynamic-row flip (Gray
-  // bit ctz(t + 8), the only column whose table row is not a compile-time constant) sits in the
-  // middle of the body, after three products its column loads can overlap, instead of at the
-  // head of the loop.  Same flips, products and additions in the same order: bit-identical.
-  template <class Cols>
-  __device__ __forceinline__ void half_walk_rot(const Cols& cols, int T0, int H, int zero) {
-    double mr = 0.0, mi = 0.0;
-    double orr = 0.0, oi = 0.0;
-    accum(row_product<N>(s), 0, mr, mi, orr, oi);             // index T0: no flip
-    for (int t = -4; t < H - 4; t += 4) {
-      const int tz = t * zero;
-      flip_row(cols, 0 + tz);                                   // r = 1: bit 0, direction 0
-      accum(row_product<N>(s), 1, mr, mi, orr, oi);
-      const int d2 = ((t + 4) >> 2) & 1;                        // r = 2: bit 1, direction bit 2 of t + 4
-      if (PERMB200_R2_XORSIGN) flip_xorsign(cols, plus_row(1) + tz, (d2 ? kSgnDir1 : kSgnDir0) < 0.0);
-      else flip_row(cols, 2 + d2 + tz);
-      accum(row_product<N>(s), 2, mr, mi, orr, oi);
-      flip_row(cols, 1 + tz);                                   // r = 3: bit 0, direction 1
-      accum(row_product<N>(s), 3, mr, mi, orr, oi);
-      if (((t + 4) & 12) == 12) {
-        if (MODE == kSep) { acc_add_sep(mr, mi, orr, oi); orr = 0.0; oi = 0.0; }
-        else acc_add(mr, mi);
-        mr = 0.0; mi = 0.0;
-      }
-      if (t + 8 < H) {                                          // r = 0 of iteration t + 4
-        const int b = (__ffs(t + 8) - 1) & 15;
-        const int d = ((T0 + t + 8) >> (b + 1)) & 1;
-        flip_row(cols, 2 * b + d);
-        accum(row_product<N>(s), 0, mr, mi, orr, oi);
       }
     }
     if (MODE == kSep) acc_add_sep(mr, mi, orr, oi);
@@ -454,11 +380,7 @@ struct Walker {
     for (int h = 0; h < 2; ++h) {
       // direction = bit c of g = bit 0 of q: per-thread sign on the +u row (uniform index)
       if (h == 1) flip_signed(cols, plus_row(c - 1), (q & 1) ? kSgnDir1 : kSgnDir0);
-#if PERMB200_R0_ROTATE
-      half_walk_rot(cols, h * H, H, zero);
-#else
       half_walk(cols, h * H, H, zero);
-#endif
     }
   }
 

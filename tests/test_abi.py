@@ -100,7 +100,7 @@ def test_custom_plan_arguments_validated_without_cuda():
     L = _lib.lib()
     buf = ctypes.create_string_buffer(64)
     f = L.perm_sweep_units_custom
-    assert f(buf, 20, 0, 4, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL      # chunk_bits < 5
+    assert f(buf, 20, 0, 3, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL      # chunk_bits < 4 (kMinFastC)
     assert f(buf, 20, 0, 13, 0, 0, 0, 1, buf, None) == _lib.PERM_EINVAL     # chunk_bits > 12
     assert f(buf, 20, 0, 10, 0, 8, 0, 1, buf, None) == _lib.PERM_EINVAL     # block_bits > 7
     assert f(buf, 20, 2, 10, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL     # dd: block_bits > 6

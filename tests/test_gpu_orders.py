@@ -160,7 +160,7 @@ def test_batched_abs2_vs_oracle_and_values():
 
 
 def test_batched_abs2_exact_on_integers():
-    As = np.stack([synth.bernoulli(12, s) for s in range(4)] + [synth.ones(10)])
+    As = np.stack([synth.bernoulli(12, s) for s in range(4)] + [synth.ones(12), synth.ones_minus_eye(12)])
     p2 = pb.glynn_batched_abs2(T(As)).cpu().numpy()
     for b in range(As.shape[0]):
         ex = oracle.exact(As[b]).value

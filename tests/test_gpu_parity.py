@@ -130,6 +130,24 @@ def test_ryser_R_or_B(n):
     check_B(got, part, n, P.chunk_bits, rel_ceiling=1e-3, what=f"ryser n={n} (rel {_rel(got, ref):.1e})")
 
 
+@pytest.mark.parametrize("n,alg", [(14, "glynn"), (20, "glynn"), (20, "ryser"), (33, "glynn")])
+def test_fast_path_smallest_chunks(n, alg):
+    """Non-canonical plans with the smallest fast-path chunk (c = kMinFastC = 4) and c = 5..7
+    against the oracle: the half-walk's direction bookkeeping at short chunks."""
+    A = synth.gaussian(n, 7100 + n)
+    dA = T(A)
+    a = pb._alg(alg)
+    m = pb.plan(n, a).log2_terms
+    for c in (4, 5, 7):
+        wb = min(7, m - c)
+        ub = m - c - wb
+        units = 1 << ub
+        for u in sorted({0, units // 2, units - 1}):
+            got = pb.sweep_units_custom(dA, a, c, 0, wb, u, u + 1).cpu().numpy()[0]
+            part = oracle.partial_ex(A, u << (c + wb), (u + 1) << (c + wb), alg)
+            check_B(complex(got[0] + got[1], got[2] + got[3]), part, n, c, what=f"{alg} n={n} c={c} unit {u}")
+
+
 # ----------------------------------------------------------------- ranges, ragged ends, partitions
 @pytest.mark.parametrize("alg", ["glynn", "ryser"])
 def test_range_partials_ragged(alg):

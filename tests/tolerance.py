@@ -49,11 +49,12 @@ def _guard(part, n: int) -> None:
             f"L1c / (n L1) = {part.l1c / (n * part.l1):.1f} above the ceiling {L1C_MAX_PER_N}: vacuous bound?"
 
 
-def record(kind: str, err: float, bound: float, ref: complex, part=None, n: int = 0, what: str = "") -> None:
+def record(kind: str, err: float, bound: float, ref: complex, part=None, n: int = 0, what: str = "",
+           scale: float = 1.0) -> None:
     REPORT.append({"test": _current_test(), "kind": kind, "what": what, "n": n, "err": err, "bound": bound,
                    "err_over_bound": err / bound if bound > 0 else (0.0 if err == 0 else math.inf),
                    "bound_over_ref": bound / abs(ref) if ref != 0 else None,
-                   "bound_factor": (bound / (U * part.l1)) if part is not None and part.l1 > 0 else None})
+                   "bound_factor": (bound / (U * part.l1 * scale)) if part is not None and part.l1 > 0 else None})
 
 
 def check_B(got: complex, part, n: int, c: int, scale: float = 1.0, *, ref: complex | None = None,
@@ -65,7 +66,7 @@ def check_B(got: complex, part, n: int, c: int, scale: float = 1.0, *, ref: comp
         ref = part.dd.to_complex() * scale
     bound = (bound_dd if dd else bound_B)(part, n, c, scale) + extra
     err = abs(got - ref)
-    record("Rdd" if dd else "B", err, bound, ref, part, n, what)
+    record("Rdd" if dd else "B", err, bound, ref, part, n, what, scale)
     if rel_ceiling is not None and ref != 0:
         assert bound <= rel_ceiling * abs(ref), f"bound / |ref| = {bound / abs(ref):.2e} > ceiling {rel_ceiling:.0e}"
     assert err <= bound + 1e-300, f"{what}: err {err:.3e} > bound {bound:.3e} (ratio {err / bound:.2f})"

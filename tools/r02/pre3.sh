@@ -1,0 +1,6 @@
+set -u
+O=gpurun_out/r02d; mkdir -p $O
+PERMB200_TOL_REPORT=$O/tol_report.json timeout 1500 python -m pytest tests -q -m gpu > $O/pytest.log 2>&1; echo "pytest rc=$?" > $O/status.txt
+for mb in 3 4 5 6 3 4 5 6; do echo "mb $mb" >> $O/batched_variants.log; timeout 120 tools/microbench/batched_bench_mb$mb 4096 >> $O/batched_variants.log 2>&1; done
+bash tools/r02/sanitize.sh; cp -r gpurun_out/r02_sanitize $O/ 2>/dev/null
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_op_write.sum,gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --cache-control all -k regex:sweep_kernel -c 1 --csv --log-file $O/sweep_m4_traffic.csv python tools/profile_sweep.py --workload M4 --fraction 1 --reps 1 > $O/traffic.log 2>&1; echo "traffic rc=$?" >> $O/status.txt
