@@ -92,22 +92,26 @@ enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_R
  * the GPU count, so any partition of the unit range reproduces the single-GPU result
  * bit for bit.
  *   terms      = 2^log2_terms (2^{n-1} Glynn, 2^n Ryser)
- *   chunk      = 2^chunk_bits consecutive Gray indices walked by one thread from a fresh
+ *   chunk      = 2^chunk_bits consecutive Gray indices walked by one leaf from a fresh
  *                O(n^2) row-sum build (the drift reset)
- *   leaf       = 2^leaf_bits chunks, walked in order by one thread into one dd accumulator
- *   unit       = 2^block_bits leaves (one thread block) -> one dd partial
+ *   leaf       = 2^leaf_bits chunks, walked in order by one group of `lanes` threads into one
+ *                dd accumulator; lanes = 1, or 4 (small n: m <= 21, n >= 8) / 2 (n >= 52,
+ *                compensated mode) with the n row sums split over the lanes
+ *   unit       = 2^block_bits leaves (one thread block of 2^block_bits * lanes threads) -> one
+ *                dd partial
  *   units      = 2^unit_bits; unit_terms = terms / units */
 typedef struct {
   int n, alg;
   int log2_terms, chunk_bits, leaf_bits, block_bits, unit_bits;
-  int reserved;
+  int lanes;
   uint64_t unit_terms;
   int64_t units;
 } perm_plan_t;
 
 /* Largest supported n (64 for Glynn; Ryser stops at 63 because its 2^n Gray indices
- * must fit in uint64).  The FP64 sweep's hot loop is spill-free up to n = 51 (row sums in
- * 4n registers); 52..64 are correct but slower (local-memory spills in the loop). */
+ * must fit in uint64).  The FP64 sweep keeps every row sum in registers for all n: one thread
+ * per chunk (4n registers) up to n = 51, two lanes per chunk (2n registers each) from 52 on
+ * (the plain and separate-addition modes keep one thread per chunk there and spill). */
 int perm_max_n(void);
 
 /* Human-readable text for a status code (for PERM_ECUDA: the last CUDA error seen by

@@ -33,7 +33,7 @@ class PermError(RuntimeError):
 class PlanT(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("alg", ctypes.c_int), ("log2_terms", ctypes.c_int),
                 ("chunk_bits", ctypes.c_int), ("leaf_bits", ctypes.c_int), ("block_bits", ctypes.c_int),
-                ("unit_bits", ctypes.c_int), ("reserved", ctypes.c_int), ("unit_terms", ctypes.c_uint64),
+                ("unit_bits", ctypes.c_int), ("lanes", ctypes.c_int), ("unit_terms", ctypes.c_uint64),
                 ("units", ctypes.c_int64)]
 
 
@@ -48,6 +48,7 @@ class Plan:
     unit_bits: int
     unit_terms: int
     units: int
+    lanes: int = 1          # threads per leaf (row-split sweeps: 4 small n, 2 for n >= 52)
 
     @property
     def terms(self) -> int:
@@ -114,7 +115,7 @@ def plan(n: int, alg: int = ALG_GLYNN) -> Plan:
     p = PlanT()
     check(lib().perm_plan(int(n), int(alg), ctypes.byref(p)), "perm_plan")
     return Plan(p.n, p.alg, p.log2_terms, p.chunk_bits, p.leaf_bits, p.block_bits, p.unit_bits,
-                int(p.unit_terms), int(p.units))
+                int(p.unit_terms), int(p.units), int(p.lanes))
 
 
 def launch_count() -> int:

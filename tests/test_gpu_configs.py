@@ -149,11 +149,13 @@ def test_m5_fast_path_units_vs_oracle(alg):
 @pytest.mark.parametrize("n", [44, 52, 53, 56, 64])
 def test_large_n_fast_path_units_vs_oracle(n):
     """Fast-path instantiations with the other register-budget choices (perm_kernels.cuh
-    acc_in_smem / product_chains; n >= 52 spills) on single-chunk custom units."""
+    acc_in_smem / product_chains at n = 44) and the 2-lane row-split sweep (n >= 52,
+    perm_kernels_split.cuh) on custom-plan units."""
     A = synth.gaussian(n, 9300 + n)
     dA = T(A)
     m = n - 1
-    c, wb = 11, 7
+    c = 11
+    wb = 7 - (pb.plan(n).lanes.bit_length() - 1)     # 2-lane leaves from n = 52: 64 per block
     lam = max(0, m - c - wb - 40)            # at most 2^40 units
     ub = m - c - wb - lam
     units = 1 << ub

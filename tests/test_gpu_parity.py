@@ -139,7 +139,7 @@ def test_fast_path_smallest_chunks(n, alg):
     a = pb._alg(alg)
     m = pb.plan(n, a).log2_terms
     for c in (4, 5, 7):
-        wb = min(7, m - c)
+        wb = min(7 - (pb.plan(n, a).lanes.bit_length() - 1), m - c)
         ub = m - c - wb
         units = 1 << ub
         for u in sorted({0, units // 2, units - 1}):

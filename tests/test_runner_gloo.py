@@ -74,7 +74,7 @@ def test_interrupted_resumed_run_is_bit_identical(tmp_path):
     assert all(c for _, _, c in res) and vals[0] == vals[1]
     ledgers = [Ledger.load(prefix + f".rank{r}.npz") for r in range(2)]
     done = sorted(int(k) for L in ledgers for k in L.seg_done)
-    assert done == list(range(128 // SEG))                      # every segment exactly once
+    assert done == list(range(-(-__import__("paper_1606_05836_b200").plan(N).units // SEG)))                      # every segment exactly once
     # reference: one process, no checkpoint
     A = torch.from_numpy(synth.gaussian(N, 321))
     ref, ok = run_checkpointed(A, "glynn", None, segment_units=SEG, sweep=oracle_sweep, combine=tree_combine)
@@ -118,7 +118,7 @@ def test_dynamic_claims_through_a_store_and_session_ledgers(tmp_path):
     files = ledger_files(prefix)
     assert len(files) == 4 and all((".s1." in f) or (".s2." in f) for f in files)
     segs = [int(k) for f in files for k in Ledger.load(f).seg_done]
-    assert sorted(segs) == list(range(128 // SEG))              # every segment exactly once
+    assert sorted(segs) == list(range(-(-__import__("paper_1606_05836_b200").plan(N).units // SEG)))              # every segment exactly once
 
 
 def test_truncated_temporary_files_are_ignored(tmp_path):

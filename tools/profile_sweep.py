@@ -27,8 +27,9 @@ ap.add_argument("--alg", default="glynn")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--batched", action="store_true")
 ap.add_argument("--custom", default="", help="c,leaf_bits,block_bits: non-canonical plan (perm_sweep_units_custom)")
+ap.add_argument("--n", type=int, default=0, help="an n x n Gaussian matrix instead of --workload")
 a = ap.parse_args()
-A = torch.from_numpy(synth.workload(a.workload)).cuda()
+A = torch.from_numpy(synth.gaussian(a.n, 9000 + a.n) if a.n else synth.workload(a.workload)).cuda()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 if a.batched:
     B, n = A.shape[0], A.shape[1]
@@ -48,7 +49,7 @@ P = pb.plan(n, alg)
 if a.custom:
     c, lam, wb = (int(x) for x in a.custom.split(","))
     ub = P.log2_terms - c - lam - wb
-    P = pb.Plan(n, alg, P.log2_terms, c, lam, wb, ub, 1 << (P.log2_terms - ub), 1 << ub)
+    P = pb.Plan(n, alg, P.log2_terms, c, lam, wb, ub, 1 << (P.log2_terms - ub), 1 << ub, P.lanes)
 units = a.units or max(1, P.units // a.fraction)
 for r in range(a.reps):
     e0.record()

@@ -57,8 +57,9 @@ out = {"n": a.n, "alg": a.alg, "canonical_plan": P.__dict__, "rows": []}
 fn_full = pb.glynn if alg == pb.ALG_GLYNN else pb.ryser
 out["canonical_full_call_us"] = graph_time(lambda: fn_full(A), a.reps)
 ref = complex(fn_full(A).item())
-for c in (3, 4, 5, 6):
-    for wb in (5, 6, 7):
+wmax = 7 - (P.lanes.bit_length() - 1)
+for c in (4, 5, 6, 7):
+    for wb in range(wmax - 2, wmax + 1):
         lam = 0
         ub = m - c - wb - lam
         if ub < 0:
@@ -67,7 +68,7 @@ for c in (3, 4, 5, 6):
         t = graph_time(lambda: pb.sweep_units_custom(A, alg, c, lam, wb, 0, units), a.reps)
         parts = pb.sweep_units_custom(A, alg, c, lam, wb, 0, units)
         v = complex(pb.combine(parts, a.n, alg)[0].item())
-        row = {"c": c, "block_bits": wb, "units": units, "threads": units << wb, "sweep_us": t,
+        row = {"c": c, "block_bits": wb, "units": units, "threads": (units << wb) * P.lanes, "sweep_us": t,
                "rel_vs_canonical": abs(v - ref) / abs(ref)}
         out["rows"].append(row)
         print(json.dumps(row), flush=True)
