@@ -63,5 +63,10 @@ cnt = P.terms >> 5
 parts = pb.sweep_units_custom(T(A), "glynn_plain", 5, 0, 0, 0, cnt)
 o = complex(pb.sum_ordered(parts, torch.from_numpy(synth.permutation(cnt, 5)).to(dev), n1, "glynn_plain").item())
 assert rel(o, ref) < 1e-7, ("ordered", o, ref)
+C = synth.gaussian(52, 52)                               # 2-lane row-split sweep (n >= 52), ragged range
+lo, hi = 12345, 12345 + (1 << 13)
+rp = oracle.partial_ex(C, lo, hi)
+gp = pb.dd_to_complex(pb.glynn_range(T(C), lo, hi))
+assert abs(gp - rp.dd.to_complex()) <= 1e-9 * rp.l1, ("split large", gp, rp.dd.to_complex())
 torch.cuda.synchronize()
 print("sanitize_cases ok", n1, n2, pb.launch_count(), "launches")
