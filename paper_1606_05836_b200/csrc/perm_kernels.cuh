@@ -160,8 +160,16 @@ __device__ __forceinline__ double2 row_product(const double2 (&s)[N]) {
 // Declared per translation unit (static): each TU stages its own copy.
 static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 
+// Batched / small kernels: keep the bit-0 step vector (used by two of every four flips) in
+// registers for the whole chunk instead of re-reading it from shared memory (A/B switch for
+// tools/microbench/batched_bench.cu).
+#ifndef PERMB200_BIT0_CACHE
+#define PERMB200_BIT0_CACHE 0
+#endif
+
 struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
+  static constexpr bool kBit0Cached = false;  // uniform LDCU operands cost no vector registers
   int base;
   __device__ __forceinline__ double2 get(int row, int i) const { return c_cols[base + row * kNMax + i]; }
 };
@@ -173,6 +181,7 @@ struct SmemColumns {
   // The batched kernel reads its columns from shared memory; with shared-memory accumulators
   // too (and their layout) M2 measured 28 % slower (1.11 vs 0.865 ms): registers there.
   static constexpr bool kSmemAccOk = false;
+  static constexpr bool kBit0Cached = PERMB200_BIT0_CACHE;
   const double2* tab;
   __device__ __forceinline__ double2 get(int row, int i) const { return tab[row * N + i]; }
 };
@@ -340,7 +349,7 @@ struct Walker {
   // LDCU (uniform operand, no vector register); other spellings of the same loop made it
   // fall back to per-thread LDC + spills (tests/test_build_sass.py guards this).
   template <class Cols>
-  __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero) {
+  __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero, const double2 (&u0)[N]) {
     double mr = 0.0, mi = 0.0;      // kSep: even-g block sums
     double orr = 0.0, oi = 0.0;     // kSep only: odd-g block sums
     for (int t = -4; t < H - 4; t += 4) {
@@ -350,7 +359,16 @@ struct Walker {
         const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
         const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
         const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
-        flip_row(cols, row);
+        if (Cols::kBit0Cached && (r & 1)) {
+          // bit 0 from registers: r = 1 adds table row 0, r = 3 row 1 = -(row 0)
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            if (r == 1) { s[i].x = __dadd_rn(s[i].x, u0[i].x); s[i].y = __dadd_rn(s[i].y, u0[i].y); }
+            else { s[i].x = __dsub_rn(s[i].x, u0[i].x); s[i].y = __dsub_rn(s[i].y, u0[i].y); }
+          }
+        } else {
+          flip_row(cols, row);
+        }
         const double2 p = row_product<N>(s);
         if (MODE == kSep) {          // parity of g = parity of r (T0 and t + 4 are multiples of 4)
           if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
@@ -374,13 +392,18 @@ struct Walker {
     const uint64_t g0 = q << c;
     build(at, g0 ^ (g0 >> 1));
     const int H = 1 << (c - 1);
+    double2 u0[N];                  // Cols::kBit0Cached: table row 0 (bit 0, direction 0)
+    if (Cols::kBit0Cached) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) u0[i] = cols.get(0, i);
+    }
     // One copy of the half-walk loop serves both halves (two inlined copies of the n = 50
     // loop body overflow the instruction cache).
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       // direction = bit c of g = bit 0 of q: per-thread sign on the +u row (uniform index)
       if (h == 1) flip_signed(cols, plus_row(c - 1), (q & 1) ? kSgnDir1 : kSgnDir0);
-      half_walk(cols, h * H, H, zero);
+      half_walk(cols, h * H, H, zero, u0);
     }
   }
 
