@@ -9,7 +9,9 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpermb200.so")
+# PERMB200_LIB selects another build of the same library (the bounds-checked debug build,
+# libpermb200_checked.so); there is no fallback of any kind.
+LIB_PATH = os.environ.get("PERMB200_LIB") or os.path.join(_HERE, "libpermb200.so")
 
 PERM_OK, PERM_EINVAL, PERM_ECUDA, PERM_ENOTIMPL = 0, 1, 2, 3
 ALG_GLYNN, ALG_RYSER, ALG_GLYNN_DD, ALG_RYSER_DD, ALG_GLYNN_PLAIN, ALG_RYSER_PLAIN = 0, 1, 2, 3, 4, 5

@@ -39,11 +39,11 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def _compile(src: str, verbose: bool) -> tuple[str, str]:
-    obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+def _compile(src: str, verbose: bool, build_dir: str = BUILD, extra=()) -> tuple[str, str]:
+    obj = os.path.join(build_dir, os.path.basename(src)[:-3] + ".o")
     if not _stale(obj, [src] + _deps()):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj + ".tmp"]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj + ".tmp"]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -53,27 +53,37 @@ def _compile(src: str, verbose: bool) -> tuple[str, str]:
     return obj, r.stderr
 
 
-def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+CHECKED_LIB = os.path.join(HERE, "libpermb200_checked.so")
+
+
+def build(force: bool = False, jobs: int | None = None, verbose: bool = False, checked: bool = False) -> str:
+    """checked=True: the bounds-checked debug build (-DPERMB200_CHECKED: device-side checks of
+    every shared-memory / table index, trap on failure) -> libpermb200_checked.so, loaded with
+    PERMB200_LIB=<path> (compute-sanitizer is not available on the GPU pool)."""
+    build_dir = BUILD + ("_checked" if checked else "")
+    lib = CHECKED_LIB if checked else LIB
+    extra = ("-DPERMB200_CHECKED",) if checked else ()
+    os.makedirs(build_dir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     if force:
-        for o in glob.glob(os.path.join(BUILD, "*.o")):
+        for o in glob.glob(os.path.join(build_dir, "*.o")):
             os.remove(o)
     jobs = jobs or max(1, min(len(srcs), os.cpu_count() or 1))
     logs = []
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = []
-        for obj, log in ex.map(lambda s: _compile(s, verbose), srcs):
+        for obj, log in ex.map(lambda s: _compile(s, verbose, build_dir, extra), srcs):
             objs.append(obj)
             if log:
                 logs.append(log)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-lcudart_static" if False else "-cudart=static"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-cudart=static"]
         subprocess.run(cmd, check=True)
-        os.replace(LIB + ".tmp", LIB)
+        os.replace(lib + ".tmp", lib)
+    LIB_OUT = lib
     if verbose:
         sys.stderr.write("\n".join(logs))
-    return LIB
+    return LIB_OUT
 
 
 if __name__ == "__main__":
@@ -81,5 +91,6 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="bounds-checked debug build")
     a = ap.parse_args()
-    print(build(a.force, a.j, a.verbose))
+    print(build(a.force, a.j, a.verbose, a.checked))

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(64) ordered_sum_kernel(const Dd2* __restrict__
       const int64_t idx = b * B + k;
       double2 v = make_double2(0.0, 0.0);
       if (idx < count) {
+        PERM_CHECK(order[idx] >= 0 && order[idx] < count);
         const Dd2 p = parts[order[idx]];
         v = make_double2(__dadd_rn(p.re_hi, p.re_lo), __dadd_rn(p.im_hi, p.im_lo));
       }

@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 namespace permb200 {
 
@@ -53,6 +54,37 @@ constexpr int kTabRows = 2 * kTabBits;   // row 2b+d = signed step vector of bit
 constexpr int kSlots = 1;      // constant-memory column slots per translation unit (32 KB each)
 constexpr int kMaxBlock = 128; // threads per block (block_bits <= 7)
 
+
+// Bounds-checked build (python -m paper_1606_05836_b200.build --checked -> libpermb200_checked.so;
+// compute-sanitizer is closed on this pool): every shared-memory table / tree / accumulator
+// access and every index that comes from device data is checked; a failed check prints the
+// condition and traps (the launch fails with cudaErrorLaunchFailure).
+#ifdef PERMB200_CHECKED
+#define PERM_CHECK(cond)                                                                     \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("permb200 check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                               \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define PERM_CHECK(cond) do { } while (0)
+#endif
+
+// Bytes of dynamic shared memory of the running launch (for PERM_CHECK of smem offsets).
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+// true if [p, p + bytes) lies inside this block's dynamic shared memory
+__device__ __forceinline__ bool in_dyn_smem(const void* p, size_t bytes) {
+  extern __shared__ double2 smem_base_[];
+  const char* b = reinterpret_cast<const char*>(smem_base_);
+  const char* q = reinterpret_cast<const char*>(p);
+  return q >= b && q + bytes <= b + dyn_smem_bytes();
+}
 
 struct Dd2 { double re_hi, re_lo, im_hi, im_lo; };
 
@@ -171,7 +203,11 @@ struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
   static constexpr bool kBit0Cached = false;  // uniform LDCU operands cost no vector registers
   int base;
-  __device__ __forceinline__ double2 get(int row, int i) const { return c_cols[base + row * kNMax + i]; }
+  __device__ __forceinline__ double2 get(int row, int i) const {
+    PERM_CHECK(row >= 0 && row < kTabRows && i >= 0 && i < kNMax && base >= 0 &&
+               base + row * kNMax + i < kSlots * kTabRows * kNMax);
+    return c_cols[base + row * kNMax + i];
+  }
 };
 
 // SmemColumns: a per-block shared-memory table with the same layout as the constant one:
@@ -183,7 +219,10 @@ struct SmemColumns {
   static constexpr bool kSmemAccOk = false;
   static constexpr bool kBit0Cached = PERMB200_BIT0_CACHE;
   const double2* tab;
-  __device__ __forceinline__ double2 get(int row, int i) const { return tab[row * N + i]; }
+  __device__ __forceinline__ double2 get(int row, int i) const {
+    PERM_CHECK(row >= 0 && row < kTabRows && i >= 0 && i < N && in_dyn_smem(tab + row * N + i, sizeof(double2)));
+    return tab[row * N + i];
+  }
 };
 
 // Plain (uncompensated) FP64 addition of two partials: the paper's accumulation
@@ -233,6 +272,7 @@ struct Walker {
     if (kSmemAcc) {
       extern __shared__ double2 smem_acc[];
       accs = reinterpret_cast<Dd2*>(smem_acc + N * N) + blockDim.x + threadIdx.x;
+      PERM_CHECK(in_dyn_smem(accs, sizeof(Dd2)));
       *accs = Dd2{0.0, 0.0, 0.0, 0.0};
     } else {
       arh = arl = aih = ail = 0.0;
@@ -524,6 +564,7 @@ __device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, 
     double2 v = A[k];
     v.x *= scale;
     v.y *= scale;
+    PERM_CHECK(in_dyn_smem(at + j * N + i, sizeof(double2)));
     at[j * N + i] = v;
   }
 }
@@ -533,6 +574,7 @@ __device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, 
 template <int MODE = kComp>
 __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  PERM_CHECK(in_dyn_smem(red + tid, sizeof(Dd2)));
   red[tid] = mine;
   __syncthreads();
   for (int o = 1; o < nt; o <<= 1) {
@@ -582,6 +624,7 @@ __device__ __forceinline__ void build_tab(const double2* at, double2* tab, int c
       const bool neg = (ALG == kGlynn) ? !d : d;
       if (neg) { v.x = -v.x; v.y = -v.y; }
     }
+    PERM_CHECK(in_dyn_smem(tab + k, sizeof(double2)));
     tab[k] = v;
   }
 }
@@ -745,6 +788,7 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
         v = at[(1 + bb) * N + i];      // 2a (pre-scaled); Glynn: d=1 -> +2a, d=0 -> -2a
         if (!d) { v.x = -v.x; v.y = -v.y; }
       }
+      PERM_CHECK(in_dyn_smem(tab + k, sizeof(double2)));
       tab[k] = v;
     }
     __syncthreads();

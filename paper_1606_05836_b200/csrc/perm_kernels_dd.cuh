@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(kDdStride, N <= kDdHiRegMax ? 4 : 1) sweep_dd_
   Dd2* red = reinterpret_cast<Dd2*>(smem + dd_smem_parts(N) * N * kDdStride);
   DdWalker<N, ALG> w;
   w.ss = smem + threadIdx.x;
+  PERM_CHECK(in_dyn_smem(w.ss + (dd_smem_parts(N) * N - 1) * kDdStride, sizeof(double2)));
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 acc{0.0, 0.0, 0.0, 0.0};

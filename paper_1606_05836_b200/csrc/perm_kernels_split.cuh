@@ -94,6 +94,7 @@ struct SplitWalker {
 
   __device__ __forceinline__ void flip_row(const double2* tab, int row) {
     const double2* t = tab + row * NP + k * NR;
+    PERM_CHECK(row >= 0 && row < kTabRows && in_dyn_smem(t, NR * sizeof(double2)));
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const double2 v = t[j];
@@ -104,6 +105,7 @@ struct SplitWalker {
 
   __device__ __forceinline__ void flip_signed(const double2* tab, int row, double sg) {
     const double2* t = tab + row * NP + k * NR;
+    PERM_CHECK(row >= 0 && row < kTabRows && in_dyn_smem(t, NR * sizeof(double2)));
 #pragma unroll
     for (int j = 0; j < NR; ++j) {
       const double2 v = t[j];
@@ -248,6 +250,7 @@ __device__ __forceinline__ void build_tab_split(const double2* at, double2* tab,
       const bool neg = (ALG == kGlynn) ? !d : d;
       if (neg) { v.x = -v.x; v.y = -v.y; }
     }
+    PERM_CHECK(in_dyn_smem(tab + idx, sizeof(double2)));
     tab[idx] = v;
   }
 }
