@@ -41,7 +41,7 @@ FIELDS = ["segment", "unit_lo", "unit_hi", "terms", "device_ms", "terms_per_s", 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--alg", default="glynn")
-    ap.add_argument("--workload", default="M5")
+    ap.add_argument("--workload", default="M5", help="a synth.WORKLOADS name, or gauss50:<n> = synth.gaussian(n, 50)")
     ap.add_argument("--ledger-in", default=os.path.join(ROOT, "runs", "m5"))
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "m5"))
     ap.add_argument("--budget-s", type=float, default=1700.0)
@@ -69,7 +69,7 @@ def main():
     # Work directory: the previous sessions' ledgers and segment logs are copied in; only THIS
     # session's files are copied to --out at the end (gpurun merges back <= 64 MiB per call,
     # while the ledgers of a 2^21-unit run total 64 MiB).
-    work = os.path.join("/tmp", f"m5work_{a.workload}_{a.alg}_{session}")
+    work = os.path.join("/tmp", f"m5work_{a.workload.replace(':', '_')}_{a.alg}_{session}")
     os.makedirs(a.out, exist_ok=True)
     if rank == 0:
         os.makedirs(work, exist_ok=True)
@@ -78,7 +78,11 @@ def main():
                 shutil.copy(f, work)
     if world > 1:
         dist.barrier()
-    A = torch.from_numpy(synth.workload(a.workload)).to(dev)
+    if a.workload.startswith("gauss50:"):
+        # the M5 family at another size (Glynn-Ryser discrepancy ladder): synth.gaussian(n, 50)
+        A = torch.from_numpy(synth.gaussian(int(a.workload.split(":")[1]), 50)).to(dev)
+    else:
+        A = torch.from_numpy(synth.workload(a.workload)).to(dev)
     n = A.shape[0]
     alg = pb._alg(a.alg)
     P = pb.plan(n, alg)
@@ -110,6 +114,13 @@ def main():
                     "rank": rank, "sm_mhz": c.get("sm_mhz"), "sm_max_mhz": c.get("sm_max_mhz"),
                     "reasons": "|".join(c.get("reasons", [])), "session": session})
         fh.flush()
+        # Mirror this session's ledger + log into --out after EVERY segment (hidden temporary
+        # name + rename): a session killed by the GPU-call time limit keeps all finished segments.
+        for src in (os.path.join(work, f"m5_{a.alg}.rank{rank}.{session}.npz"), seg_csv):
+            if os.path.exists(src):
+                tmp = os.path.join(a.out, ".tmp-" + os.path.basename(src))
+                shutil.copy(src, tmp)
+                os.replace(tmp, os.path.join(a.out, os.path.basename(src)))
 
     deadline = t_start + a.budget_s
     val, done = run_checkpointed(A, alg, os.path.join(work, f"m5_{a.alg}"), segment_units=a.segment_units,

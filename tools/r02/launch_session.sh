@@ -11,4 +11,5 @@ for f in gpurun_out/m5r/m5_ryser.rank*.npz gpurun_out/m5r/segments.rank*.csv; do
 done
 ls runs/m5r | grep -c npz
 P=""; [ "$PRE" != "-" ] && P="bash $PRE"
-exec /usr/local/graft/bin/gpurun --timeout $((TOTAL + 600)) -- "bash tools/r02/ryser_session.sh $TOTAL \"$P\""
+TO=$((TOTAL + 300)); [ $TO -gt 3600 ] && TO=3600   # gpurun clamps a call to 3600 s
+exec /usr/local/graft/bin/gpurun --timeout $TO -- "bash tools/r02/ryser_session.sh $TOTAL \"$P\""
