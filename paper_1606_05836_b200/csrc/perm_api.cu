@@ -86,8 +86,7 @@ constexpr int kAlgs = 8;
 SweepLauncher g_sweep[kAlgs][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN, GLYNN_SEP, RYSER_SEP
 SweepLauncher g_small[kAlgs][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
 FusedLauncher g_small_fused[kAlgs][kNMax + 1];   // the same + grid barrier + combine, one launch
-SweepLauncher g_split[kAlgs][kNMax + 1];   // row-split sweep (perm_kernels_split.cuh): small n, n >= 52
-FusedLauncher g_split_fused[kAlgs][kNMax + 1];
+SweepLauncher g_split[kAlgs][kNMax + 1];   // row-split sweep (perm_kernels_split.cuh): n >= 52
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -118,7 +117,6 @@ void init_tables() {
     register_sep_ryser_b(g_sweep[PERM_ALG_RYSER_SEP]);
     register_small(g_small);
     register_small_fused(g_small_fused);
-    register_split_small(g_split, g_split_fused);
     register_split_large(g_split);
     register_batched_a(g_batched);
     register_batched_b(g_batched);
@@ -143,19 +141,21 @@ int mode_of(int alg) { return is_plain(alg) ? kPlain : is_sep(alg) ? kSep : kCom
 // the one subtraction of separate addition: even - odd, times (-1)^n for Ryser (Eq. (1))
 int sep_sign(int n, int alg) { return !is_sep(alg) ? 0 : (!is_glynn(alg) && (n & 1)) ? -1 : 1; }
 
-// Lanes per chunk (leaf) of the FP64 sweep: 4 for small n (m <= kSmallLog2, n >= 8; latency-
-// bound with one thread per chunk), 2 for n >= kSplitLargeN in the compensated mode (4n row-sum
-// registers do not fit one thread), else 1 (perm_kernels_split.cuh).
-constexpr int kSplitSmallMinN = 8;
+// Lanes per chunk (leaf) of the FP64 sweep: 2 for n >= kSplitLargeN in the compensated mode (4n
+// row-sum registers do not fit one thread), else 1 (perm_kernels_split.cuh).  Small n (m <=
+// kSmallLog2) walks one thread per chunk with double-buffered row sums (SmemColumns DB): the
+// 4-lane split measured slower on M1 (n = 20: 26.7 / 47.2 us per Glynn / Ryser call against
+// 18.5 / 22.6 us for one lane, profiles/r02_m1_latency_split4.log) -- at ~1 warp per scheduler the
+// FP64 pipe, not the per-thread chain, bounds it, and the split adds shuffles and a combine cmul.
 constexpr int kSplitLargeN = 52;
 int split_lanes(int n, int alg) {
   if (is_dd(alg)) return 1;
   const int m = is_glynn(alg) ? n - 1 : n;
-  if (m <= kSmallLog2) return n >= kSplitSmallMinN ? 4 : 1;
+  if (m <= kSmallLog2) return 1;
   if (n >= kSplitLargeN && mode_of(alg) == kComp) return 2;
   return 1;
 }
-int lanes_log2(int R) { return R == 4 ? 2 : R == 2 ? 1 : 0; }
+int lanes_log2(int R) { return R == 2 ? 1 : 0; }
 
 void make_plan(int n, int alg, perm_plan_t* p) {
   const int m = is_glynn(alg) ? n - 1 : n;
@@ -166,14 +166,6 @@ void make_plan(int n, int alg, perm_plan_t* p) {
   int wbits, c, ubits, lam;
   if (m < 5) {
     wbits = 0; c = m; ubits = 0; lam = 0;      // tiny: one thread, generic walk
-  } else if (R == 4) {
-    // small n, row-split: 32-term chunks (the per-thread chain is the latency), units <= 2^10
-    // (the fused launch's final reduce and co-residency)
-    wbits = m - 5 < wmax ? m - 5 : wmax;
-    c = m - wbits - 10 > 5 ? m - wbits - 10 : 5;
-    if (c > m - wbits) c = m - wbits;
-    ubits = m - wbits - c;
-    lam = 0;
   } else {
     wbits = m - 5 < wmax ? m - 5 : wmax;
     const int rem = m - wbits;
@@ -374,31 +366,8 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
   const uint64_t T = 1ULL << P.log2_terms;
   int rc = -1;
   init_tables();
-  const FusedLauncher split_fused = P.lanes > 1 ? g_split_fused[alg][n] : nullptr;
-  if (split_fused && P.units <= (8LL << P.block_bits) * P.lanes) {
-    // small n, row-split: sweep + combine in one cooperative launch (same bits as the
-    // two-kernel path); if the grid cannot be co-resident, the two launches below
-    SweepArgs a;
-    a.A = reinterpret_cast<const double2*>(A);
-    a.unit_out = parts;
-    a.lo = 0; a.hi = T;
-    a.unit_lo = 0;
-    a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
-    a.slot = 0; a.col_base = 0; a.zero = 0;
-    const FinishArgs f{reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), is_glynn(alg) ? 1 : 0,
-                       -(n - 1), 1, sep_sign(n, alg)};
-    cudaError_t le = split_fused(a, f, P.units, st);
-    if (le == cudaSuccess) {
-      rc = PERM_OK;
-      note_launch();
-    } else if (le != cudaErrorCooperativeLaunchTooLarge) {
-      rc = cuda_fail(le, "fused split launch");
-    }
-  }
-  if (rc != -1) {
-    // done (or failed) above
-  } else if (P.lanes == 1 && !is_dd(alg) && P.log2_terms <= kSmallLog2 && g_small_fused[alg][n] &&
-             P.units <= (8LL << P.block_bits)) {
+  if (P.lanes == 1 && !is_dd(alg) && P.log2_terms <= kSmallLog2 && g_small_fused[alg][n] &&
+      P.units <= (8LL << P.block_bits)) {
     // small n: sweep + combine in one cooperative launch (same bits as the two-kernel path)
     SweepArgs a;
     a.A = reinterpret_cast<const double2*>(A);
@@ -410,9 +379,16 @@ int full_perm(const perm_c128* A, int n, int alg, perm_c128* out, cudaStream_t s
     const FinishArgs f{reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), is_glynn(alg) ? 1 : 0,
                        -(n - 1), 1, sep_sign(n, alg)};
     cudaError_t le = g_small_fused[alg][n](a, f, P.units, st);
-    rc = le == cudaSuccess ? PERM_OK : cuda_fail(le, "fused small launch");
-    if (rc == PERM_OK) note_launch();
-  } else {
+    if (le == cudaSuccess) {
+      rc = PERM_OK;
+      note_launch();
+    } else if (le != cudaErrorCooperativeLaunchTooLarge) {
+      rc = cuda_fail(le, "fused small launch");
+    }
+    // cudaErrorCooperativeLaunchTooLarge: the grid cannot be co-resident (another kernel owns
+    // the SMs' registers / shared memory): the same sweep + combine as two launches below
+  }
+  if (rc == -1) {
     rc = run_sweep(A, P, 0, P.units, 0, T, parts, staging, st);
     if (rc == PERM_OK)
       rc = run_combine(parts, P.units, n, alg, reinterpret_cast<double2*>(out), reinterpret_cast<Dd2*>(out_dd), st, 1);

@@ -72,6 +72,34 @@ constexpr int kMaxBlock = 128; // threads per block (block_bits <= 7)
 #define PERM_CHECK(cond) do { } while (0)
 #endif
 
+// Phase timers (tools/microbench/m1_phases.cu only; compiled out of the library): block-level
+// timestamps of the fused small-n kernel -- slot k holds the max over blocks of the %globaltimer
+// value at the end of phase k (slot 0: the min at kernel entry), slots 8+k the sum over blocks
+// of the block's clock64 cycles spent in phase k.
+#ifdef PERMB200_PHASE_TIMES
+__device__ unsigned long long g_phase[16];
+__device__ __forceinline__ unsigned long long perm_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PERM_PHASE_START(var)                                                      \
+  long long var = clock64();                                                       \
+  if (threadIdx.x == 0) atomicMin(&g_phase[0], perm_gtimer())
+#define PERM_PHASE(k, var)                                                         \
+  do {                                                                             \
+    if (threadIdx.x == 0) {                                                        \
+      const long long now_ = clock64();                                            \
+      atomicMax(&g_phase[k], perm_gtimer());                                       \
+      atomicAdd(&g_phase[8 + (k)], (unsigned long long)(now_ - var));              \
+      var = now_;                                                                  \
+    }                                                                              \
+  } while (0)
+#else
+#define PERM_PHASE_START(var) do { } while (0)
+#define PERM_PHASE(k, var) do { } while (0)
+#endif
+
 // Bytes of dynamic shared memory of the running launch (for PERM_CHECK of smem offsets).
 __device__ __forceinline__ unsigned dyn_smem_bytes() {
   unsigned r;
@@ -201,6 +229,7 @@ static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 
 struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
+  static constexpr bool kDoubleBuffer = false;
   static constexpr bool kBit0Cached = false;  // uniform LDCU operands cost no vector registers
   int base;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -212,11 +241,18 @@ struct ConstColumns {
 
 // SmemColumns: a per-block shared-memory table with the same layout as the constant one:
 // tab[(2b+d)*N + i] = signed step vector of Gray bit b, direction d (zero rows for b >= c).
-template <int N>
+// Double-buffered row sums (small single permanents, DB = true): the flip of step t writes the
+// OTHER register copy of the row sums, s' = s + u, instead of updating s in place, so the
+// product of term t and the flip + product of term t+1 are independent instruction streams
+// (2x the ILP of a latency-bound walker: M1 runs ~1 warp per scheduler).  Each flip is the same
+// DADD of the same operands and every product the same row_product<N>, so the terms -- and the
+// results -- are bit-identical to the in-place walk.  Costs 4n more registers: small n only.
+template <int N, bool DB = false>
 struct SmemColumns {
   // The batched kernel reads its columns from shared memory; with shared-memory accumulators
   // too (and their layout) M2 measured 28 % slower (1.11 vs 0.865 ms): registers there.
   static constexpr bool kSmemAccOk = false;
+  static constexpr bool kDoubleBuffer = DB;
   static constexpr bool kBit0Cached = PERMB200_BIT0_CACHE;
   const double2* tab;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -388,6 +424,57 @@ struct Walker {
   // column indices.  ptxas then keeps t in a uniform register and reads the columns with
   // LDCU (uniform operand, no vector register); other spellings of the same loop made it
   // fall back to per-thread LDC + spills (tests/test_build_sass.py guards this).
+  // Double-buffered half-walk (Cols::kDoubleBuffer): the same steps, flips, products, signs and
+  // 16-term blocks as half_walk below, with step r writing the row sums into the other copy
+  // (r even: s -> s2, r odd: s2 -> s; four steps per iteration end in s).
+  // The opaque tz = t*zero in the loop-invariant row indices (as in half_walk) keeps ptxas from
+  // hoisting those rows' loads out of the loop into registers (which spilled).
+  template <class Cols>
+  __device__ __forceinline__ void half_walk_db(const Cols& cols, int T0, int H, int zero) {
+    double2 s2[N];
+    double mr = 0.0, mi = 0.0;
+    double orr = 0.0, oi = 0.0;
+    for (int t = -4; t < H - 4; t += 4) {
+      const int tz = t * zero;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
+        const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
+        const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
+        double2 p;
+        if ((r & 1) == 0) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const double2 v = cols.get(row, i);
+            s2[i].x = __dadd_rn(s[i].x, v.x);
+            s2[i].y = __dadd_rn(s[i].y, v.y);
+          }
+          p = row_product<N>(s2);
+        } else {
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            const double2 v = cols.get(row, i);
+            s[i].x = __dadd_rn(s2[i].x, v.x);
+            s[i].y = __dadd_rn(s2[i].y, v.y);
+          }
+          p = row_product<N>(s);
+        }
+        if (MODE == kSep) {
+          if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
+          else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
+        } else if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
+        else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
+      }
+      if (((t + 4) & 12) == 12) {
+        if (MODE == kSep) { acc_add_sep(mr, mi, orr, oi); orr = 0.0; oi = 0.0; }
+        else acc_add(mr, mi);
+        mr = 0.0; mi = 0.0;
+      }
+    }
+    if (MODE == kSep) acc_add_sep(mr, mi, orr, oi);
+    else acc_add(mr, mi);
+  }
+
   template <class Cols>
   __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero, const double2 (&u0)[N]) {
     double mr = 0.0, mi = 0.0;      // kSep: even-g block sums
@@ -443,7 +530,8 @@ struct Walker {
     for (int h = 0; h < 2; ++h) {
       // direction = bit c of g = bit 0 of q: per-thread sign on the +u row (uniform index)
       if (h == 1) flip_signed(cols, plus_row(c - 1), (q & 1) ? kSgnDir1 : kSgnDir0);
-      half_walk(cols, h * H, H, zero, u0);
+      if (Cols::kDoubleBuffer) half_walk_db(cols, h * H, H, zero);
+      else half_walk(cols, h * H, H, zero, u0);
     }
   }
 
@@ -635,6 +723,12 @@ __device__ __forceinline__ void build_tab(const double2* at, double2* tab, int c
 // launches (this + combine) instead of four.  The terms and their order are the sweep
 // kernel's (same table values, same flips, same accumulation), i.e. bit-identical results.
 constexpr int kSmallLog2 = 21;
+// Small single permanents walk with double-buffered row sums (SmemColumns DB) up to this n
+// (8n registers of row sums).
+#ifndef PERMB200_SMALL_DB
+#define PERMB200_SMALL_DB 1
+#endif
+__host__ __device__ constexpr bool small_double_buffer(int N) { return PERMB200_SMALL_DB && N <= 22; }
 
 template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs args) {
@@ -647,7 +741,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs 
   __syncthreads();
   build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
   __syncthreads();
-  const SmemColumns<N> cols{tab};
+  const SmemColumns<N, small_double_buffer(N)> cols{tab};
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   const int ubits = args.block_bits + args.lam + args.c;
@@ -719,22 +813,28 @@ __device__ __forceinline__ void finish_root(const Dd2& r, const FinishArgs& f) {
 template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const SweepArgs args, const FinishArgs fin) {
   extern __shared__ double2 smem[];
+  PERM_PHASE_START(ph_t);
   double2* at = smem;
   double2* tab = smem + N * N;
   Dd2* red = reinterpret_cast<Dd2*>(smem + N * N + kTabRows * N);
   stage_transposed<N>(args.A, at, Walker<N, ALG>::kScale);
   __syncthreads();
+  PERM_PHASE(1, ph_t);
   build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
   __syncthreads();
-  const SmemColumns<N> cols{tab};
+  PERM_PHASE(2, ph_t);
+  const SmemColumns<N, small_double_buffer(N)> cols{tab};
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 mine;
   if (args.c >= kMinFastC) mine = walk_leaf<N, ALG, true, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
   else mine = walk_leaf<N, ALG, false, MODE>(cols, at, leaf_id, args.c, args.lam, args.lo, args.hi, args.zero);
+  PERM_PHASE(3, ph_t);
   block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
+  PERM_PHASE(4, ph_t);
   cooperative_groups::this_grid().sync();
+  PERM_PHASE(5, ph_t);
   if (blockIdx.x == 0) {
     // units (a power of two) <= 8 * blockDim: thread t first reduces the aligned segment
     // [t S, (t+1) S) (the bottom levels of the canonical tree), then the block tree
@@ -752,6 +852,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
     const Dd2 v = stack[top];
     block_tree<MODE>(red, v);
     if (threadIdx.x == 0) finish_root(red[0], fin);
+    PERM_PHASE(6, ph_t);
   }
 }
 
@@ -877,6 +978,20 @@ cudaError_t launch_sweep_small_fused(const SweepArgs& a, const FinishArgs& f, in
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
+  // every block of a cooperative launch must be co-resident: resident blocks per SM x SMs,
+  // computed once per instantiation (and block size) -- one device model per process
+  static int cap_threads = 0, cap_blocks = 0;
+  if (cap_threads != threads) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep_small_fused_kernel<N, ALG, MODE>,
+                                                                  threads, smem);
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    cap_blocks = per_sm * sms;
+    cap_threads = threads;
+  }
+  if (cap_blocks < units) return cudaErrorCooperativeLaunchTooLarge;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)units);
   cfg.blockDim = dim3((unsigned)threads);

@@ -1,24 +1,23 @@
 // perm_kernels_split.cuh — the Gray-code sweep with each chunk's n row sums SPLIT over a group
-// of R consecutive lanes (R = 4 for small n, R = 2 for n >= 52).  Included by the
-// perm_inst_split_*.cu translation units after perm_kernels.cuh.
+// of R = 2 consecutive lanes, for n >= 52.  Included by perm_inst_split_large.cu after
+// perm_kernels.cuh.
 //
 // Same method as perm_kernels.cuh (Eq. (2) P:66-68 / Eq. (1), walked in Gray-code
 // order, one +-column update and one n-way product per term), different mapping:
 //   * lane k of a group holds rows [k NR, (k+1) NR) (NR = ceil(n / R); rows >= n are padding
 //     fixed at 1 + 0i, an exact multiplicative identity of cmul), flips only those rows and
 //     multiplies them into a lane partial product;
-//   * the group combines the lane partials with one (R = 2) or two (R = 4) shuffle levels,
-//     always as cmul(lower lanes, upper lanes), so every lane ends with the same, uniquely
-//     ordered term ((p0 p1)(p2 p3)); every lane accumulates it (the accumulators of a group
-//     are identical) and only lane 0 feeds the block tree (the others contribute exact zeros,
-//     so the tree over threads equals the canonical tree over leaves = groups);
+//   * the group combines the lane partials with shuffles, always as cmul(lower lanes, upper
+//     lanes), so every lane ends with the same, uniquely ordered term; every lane accumulates it
+//     (the accumulators of a group are identical) and only lane 0 feeds the block tree (the
+//     others contribute exact zeros, so the tree over threads equals the canonical tree over
+//     leaves = groups);
 //   * the step vectors come from a per-block shared-memory table with the padded row stride
 //     NP = R NR: a warp reads R distinct addresses per flip (one wavefront).
-// Why: small n (M1, n = 20: 2^19 terms) is latency-bound with one thread per chunk -- 128
-// blocks of 4 warps, one warp per scheduler, every dependency exposed (11.7 us sweep, r02 M1
-// plan sweep); four lanes per chunk give 4x the warps with a quarter of the per-thread chain
-// and of the O(n^2) chunk build.  Large n (>= 52) exceeds the register file with 4n registers
-// of row sums (local-memory spills); two lanes hold 2n registers each.
+// Why: from n = 52, 4n registers of row sums exceed what one thread can hold next to the
+// product chains (round 1: local-memory spills in the hot loop); two lanes hold 2n each.  (A
+// 4-lane variant for small n was measured slower than one lane per chunk on M1 and removed:
+// profiles/r02_m1_latency_split4.log.)
 #pragma once
 
 #include "perm_kernels.cuh"
@@ -256,10 +255,8 @@ __device__ __forceinline__ void build_tab_split(const double2* at, double2* tab,
 }
 
 // One block = one unit of the canonical plan: 2^block_bits leaves (groups) x R lanes.
-// FUSED (small n): cooperative grid barrier, block 0 reduces the unit partials with the
-// canonical tree and finishes (as sweep_small_fused_kernel).
-template <int N, int ALG, int MODE, int R, bool FUSED>
-__global__ void __launch_bounds__(kMaxBlock) sweep_split_kernel(const SweepArgs args, const FinishArgs fin) {
+template <int N, int ALG, int MODE, int R>
+__global__ void __launch_bounds__(kMaxBlock) sweep_split_kernel(const SweepArgs args) {
   constexpr int NR = split_rows(N, R), NP = NR * R;
   extern __shared__ double2 smem[];
   // [N*N: at][kTabRows*NP: tab][blockDim Dd2: tree]
@@ -293,23 +290,6 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_split_kernel(const SweepArgs 
   const Dd2 mine = (k == 0) ? acc : Dd2{0.0, 0.0, 0.0, 0.0};
   block_tree<MODE>(red, mine);
   if (threadIdx.x == 0) args.unit_out[blockIdx.x] = red[0];
-  if (!FUSED) return;
-  cooperative_groups::this_grid().sync();
-  if (blockIdx.x == 0) {
-    const int S = gridDim.x > blockDim.x ? (int)(gridDim.x / blockDim.x) : 1;
-    Dd2 stack[4];
-    int top = 0;
-    for (int kk = 0; kk < S; ++kk) {
-      const unsigned idx = threadIdx.x * S + kk;
-      Dd2 v = idx < gridDim.x ? args.unit_out[idx] : Dd2{0.0, 0.0, 0.0, 0.0};
-      int lvl = 0;
-      for (int m = kk; m & 1; m >>= 1) { v = part_add<MODE>(stack[lvl], v); ++lvl; }
-      stack[lvl] = v;
-      if (lvl > top) top = lvl;
-    }
-    block_tree<MODE>(red, stack[top]);
-    if (threadIdx.x == 0) finish_root(red[0], fin);
-  }
 }
 
 template <int N, int R>
@@ -322,41 +302,12 @@ cudaError_t launch_split(const SweepArgs& a, int64_t units, double2*, cudaStream
   const int threads = (1 << a.block_bits) * R;
   const size_t smem = split_smem<N, R>(threads);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(sweep_split_kernel<N, ALG, MODE, R, false>,
+    cudaError_t e = cudaFuncSetAttribute(sweep_split_kernel<N, ALG, MODE, R>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  sweep_split_kernel<N, ALG, MODE, R, false><<<(unsigned)units, threads, smem, st>>>(a, FinishArgs{});
+  sweep_split_kernel<N, ALG, MODE, R><<<(unsigned)units, threads, smem, st>>>(a);
   return cudaGetLastError();
-}
-
-template <int N, int ALG, int MODE, int R>
-cudaError_t launch_split_fused(const SweepArgs& a, const FinishArgs& f, int64_t units, cudaStream_t st) {
-  const int threads = (1 << a.block_bits) * R;
-  const size_t smem = split_smem<N, R>(threads);
-  auto kern = sweep_split_kernel<N, ALG, MODE, R, true>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  // every block of a cooperative launch must be co-resident
-  int per_sm = 0, dev = 0, sms = 0;
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e != cudaSuccess) return e;
-  if ((int64_t)per_sm * sms < units) return cudaErrorCooperativeLaunchTooLarge;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)units);
-  cfg.blockDim = dim3((unsigned)threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, f);
 }
 
 }  // namespace permb200
@@ -366,9 +317,5 @@ namespace permb200 {
 template <int ALG, int MODE, int R, int LO, int... Is>
 void fill_split(SweepLauncher* table, std::integer_sequence<int, Is...>) {
   ((table[LO + Is] = &launch_split<LO + Is, ALG, MODE, R>), ...);
-}
-template <int ALG, int MODE, int R, int LO, int... Is>
-void fill_split_fused(FusedLauncher* table, std::integer_sequence<int, Is...>) {
-  ((table[LO + Is] = &launch_split_fused<LO + Is, ALG, MODE, R>), ...);
 }
 }  // namespace permb200

@@ -103,7 +103,6 @@ def test_custom_plan_arguments_validated_without_cuda():
     assert f(buf, 20, 0, 3, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL      # chunk_bits < 4 (kMinFastC)
     assert f(buf, 20, 0, 13, 0, 0, 0, 1, buf, None) == _lib.PERM_EINVAL     # chunk_bits > 12
     assert f(buf, 30, 0, 10, 0, 8, 0, 1, buf, None) == _lib.PERM_EINVAL     # block_bits > 7
-    assert f(buf, 20, 0, 10, 0, 6, 0, 1, buf, None) == _lib.PERM_EINVAL     # 4-lane leaves: block_bits > 5
     assert f(buf, 56, 0, 10, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL     # 2-lane leaves: block_bits > 6
     assert f(buf, 20, 2, 10, 0, 7, 0, 1, buf, None) == _lib.PERM_EINVAL     # dd: block_bits > 6
     assert f(buf, 20, 0, 10, 5, 5, 0, 1, buf, None) == _lib.PERM_EINVAL     # c + lam + wb > 19
