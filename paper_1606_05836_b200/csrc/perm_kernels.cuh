@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
 // blocks/SM, 9.2 waves for M2's 4096 permanents; ncu profiles/r01_batched_m2_*) leaves warps
 // idle.  At 4 blocks (<= 128 registers) chunk_fast<16> still has no spills (only the kernel
 // body spills a few values across the chunk call).
+#ifndef PERMB200_BATCHED_DB           // A/B: double-buffered row sums in the batched walk
+#define PERMB200_BATCHED_DB false
+#endif
 #ifdef PERMB200_BATCHED_MINB          // A/B experiments (tools/microbench/batched_bench.cu)
 __host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? PERMB200_BATCHED_MINB : N <= 20 ? 3 : 1; }
 #else
@@ -893,7 +896,7 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
       tab[k] = v;
     }
     __syncthreads();
-    const SmemColumns<N> cols{tab};
+    const SmemColumns<N, PERMB200_BATCHED_DB> cols{tab};
     const uint64_t terms = 1ull << (N - 1);
     Dd2 mine;
     if (args.c >= kMinFastC) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
