@@ -223,6 +223,10 @@ static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 // Batched / small kernels: keep the bit-0 step vector (used by two of every four flips) in
 // registers for the whole chunk instead of re-reading it from shared memory (A/B switch for
 // tools/microbench/batched_bench.cu).
+#ifndef PERMB200_ROW_AHEAD             // A/B switch (tools/microbench/sweep_bench.cu)
+#define PERMB200_ROW_AHEAD 1
+#endif
+__host__ __device__ constexpr bool row_ahead(int N) { return PERMB200_ROW_AHEAD && (N <= 46 || N == 49); }
 #ifndef PERMB200_BIT0_CACHE
 #define PERMB200_BIT0_CACHE 0
 #endif
@@ -475,17 +479,34 @@ struct Walker {
     else acc_add(mr, mi);
   }
 
+  // Row of the step-r = 0 flip into local index T0 + t + 4: Gray bit b = ctz(t + 4) (t = -4: bit
+  // 15, an all-zero table row), direction bit b + 1 of the index.
+  static __device__ __forceinline__ int head_row(int T0, int t) {
+    const int b = (__ffs(t + 4) - 1) & 15;
+    return 2 * b + (((T0 + t + 4) >> (b + 1)) & 1);
+  }
+
   template <class Cols>
   __device__ __forceinline__ void half_walk(const Cols& cols, int T0, int H, int zero, const double2 (&u0)[N]) {
     double mr = 0.0, mi = 0.0;      // kSep: even-g block sums
     double orr = 0.0, oi = 0.0;     // kSep only: odd-g block sums
+    // PERMB200_ROW_AHEAD: the step-0 row of the NEXT iteration is computed during this one (a
+    // loop-carried uniform value), so the loop head's column loads do not wait behind the
+    // ctz / shift chain (ncu source view, n = 50: the runtime-row flips at steps 0 and 2 carried
+    // ~all of the short-scoreboard stalls; the constant-row bit-0 flips none).
+    // Per n (spill-free SASS only, tools/sass_loop_stats.py: on for n <= 46 and n = 49; at n = 48,
+    // 50, 51 the extra live value tipped ptxas into spills).
+    constexpr bool kAhead = row_ahead(N);
+    int row0_next = head_row(T0, -4);
     for (int t = -4; t < H - 4; t += 4) {
       const int tz = t * zero;
+      const int row0 = row0_next;
+      if (kAhead) row0_next = head_row(T0, t + 4);
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
         const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
-        const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
+        const int row = (r == 0) ? (kAhead ? row0 : 2 * b + d) : (2 * b + d + tz);
         if (Cols::kBit0Cached && (r & 1)) {
           // bit 0 from registers: r = 1 adds table row 0, r = 3 row 1 = -(row 0)
 #pragma unroll
