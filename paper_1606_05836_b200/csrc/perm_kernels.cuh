@@ -189,8 +189,11 @@ __device__ __forceinline__ Dd2 dd2_add(const Dd2& a, const Dd2& b) {
 //     4 chains, 32 / 2 with 3);  n = 51: smem + 3: 10 / 0;  n = 52: registers + 3: 68 / 28;
 //   n = 53: smem + 3: 192 / 20;  n >= 54: registers + 2: 70 / 16 (n = 54) .. 184 / 40 (56).
 __host__ __device__ constexpr bool acc_in_smem(int N) { return N <= 51 || N == 53; }
+#ifndef PERMB200_N50_CHAINS            // A/B switch for the M5 size (tools/microbench/sweep_bench.cu)
+#define PERMB200_N50_CHAINS 4
+#endif
 __host__ __device__ constexpr int product_chains(int N) {
-  return N < 4 ? N : N <= 50 ? 4 : N <= 53 ? 3 : 2;
+  return N == 50 ? PERMB200_N50_CHAINS : N < 4 ? N : N <= 50 ? 4 : N <= 53 ? 3 : 2;
 }
 
 // Product of the n row sums: NC independent chains (i mod NC) then a pairwise tree.
@@ -226,7 +229,12 @@ static __constant__ double2 c_cols[kSlots * kTabRows * kNMax];
 #ifndef PERMB200_ROW_AHEAD             // A/B switch (tools/microbench/sweep_bench.cu)
 #define PERMB200_ROW_AHEAD 1
 #endif
-__host__ __device__ constexpr bool row_ahead(int N) { return PERMB200_ROW_AHEAD && (N <= 46 || N == 49); }
+#ifndef PERMB200_N50_AHEAD
+#define PERMB200_N50_AHEAD 0
+#endif
+__host__ __device__ constexpr bool row_ahead(int N) {
+  return PERMB200_ROW_AHEAD && (N <= 46 || N == 49 || (N == 50 && PERMB200_N50_AHEAD));
+}
 #ifndef PERMB200_BIT0_CACHE
 #define PERMB200_BIT0_CACHE 0
 #endif
