@@ -189,6 +189,13 @@ __device__ __forceinline__ Dd2 dd2_add(const Dd2& a, const Dd2& b) {
 //     4 chains, 32 / 2 with 3);  n = 51: smem + 3: 10 / 0;  n = 52: registers + 3: 68 / 28;
 //   n = 53: smem + 3: 192 / 20;  n >= 54: registers + 2: 70 / 16 (n = 54) .. 184 / 40 (56).
 __host__ __device__ constexpr bool acc_in_smem(int N) { return N <= 51 || N == 53; }
+// Chunk-start build shape (Walker::build): rows per pass and columns per loop iteration.
+#ifndef PERMB200_SMALL_BUILD          // A/B switch (tools/microbench/m1_phases.cu)
+#define PERMB200_SMALL_BUILD 1
+#endif
+__host__ __device__ constexpr int build_rows(int N) { return (PERMB200_SMALL_BUILD && N <= 24) ? N : 8; }
+__host__ __device__ constexpr int build_col_unroll(int N) { return (PERMB200_SMALL_BUILD && N <= 24) ? 2 : 1; }
+
 #ifndef PERMB200_N50_CHAINS            // A/B switch for the M5 size (tools/microbench/sweep_bench.cu)
 #define PERMB200_N50_CHAINS 4
 #endif
@@ -241,7 +248,6 @@ __host__ __device__ constexpr bool row_ahead(int N) {
 
 struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
-  static constexpr bool kDoubleBuffer = false;
   static constexpr bool kBit0Cached = false;  // uniform LDCU operands cost no vector registers
   int base;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -253,18 +259,11 @@ struct ConstColumns {
 
 // SmemColumns: a per-block shared-memory table with the same layout as the constant one:
 // tab[(2b+d)*N + i] = signed step vector of Gray bit b, direction d (zero rows for b >= c).
-// Double-buffered row sums (small single permanents, DB = true): the flip of step t writes the
-// OTHER register copy of the row sums, s' = s + u, instead of updating s in place, so the
-// product of term t and the flip + product of term t+1 are independent instruction streams
-// (2x the ILP of a latency-bound walker: M1 runs ~1 warp per scheduler).  Each flip is the same
-// DADD of the same operands and every product the same row_product<N>, so the terms -- and the
-// results -- are bit-identical to the in-place walk.  Costs 4n more registers: small n only.
-template <int N, bool DB = false>
+template <int N>
 struct SmemColumns {
   // The batched kernel reads its columns from shared memory; with shared-memory accumulators
   // too (and their layout) M2 measured 28 % slower (1.11 vs 0.865 ms): registers there.
   static constexpr bool kSmemAccOk = false;
-  static constexpr bool kDoubleBuffer = DB;
   static constexpr bool kBit0Cached = PERMB200_BIT0_CACHE;
   const double2* tab;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -370,9 +369,13 @@ struct Walker {
 
   // Chunk-start row sums for code G ("Convert iter to the set delta ...
   // Calculate s"), O(n^2), from the transposed, pre-scaled matrix in shared memory.  Rows are done
-  // 8 at a time with a runtime column loop, which bounds the registers the loads take.
+  // RB at a time with a runtime column loop, which bounds the registers the loads take: 8 rows
+  // for large n; all rows, two columns per iteration, for n <= 24, where the build is a large
+  // share of a chunk (M1: 32-term chunks) and was bound by the shared-memory load latency of
+  // each 8-row column slice (m1_phases: ~6000 of the walk's 15500 cycles per block).  Every row
+  // sum is accumulated over the same columns in the same order: the same bits either way.
   __device__ __forceinline__ void build(const double2* __restrict__ at, uint64_t G) {
-    constexpr int RB = 8;
+    constexpr int RB = build_rows(N);
 #pragma unroll
     for (int r0 = 0; r0 < N; r0 += RB) {
 #pragma unroll
@@ -381,7 +384,7 @@ struct Walker {
           if (ALG == kGlynn) s[i] = make_double2(0.5 * at[i].x, 0.5 * at[i].y);  // delta_1 = +1; exact
           else s[i] = make_double2(0.0, 0.0);          // Ryser: S starts empty
         }
-#pragma unroll 1
+#pragma unroll (build_col_unroll(N))
       for (int j = (ALG == kGlynn) ? 1 : 0; j < N; ++j) {
         const int bit = (ALG == kGlynn) ? (int)((G >> (j - 1)) & 1) : (int)((G >> j) & 1);
         // at holds kScale * a: weight delta_j / 2 (Glynn) reproduces RN(s + delta_j a_ij) exactly
@@ -436,57 +439,6 @@ struct Walker {
   // column indices.  ptxas then keeps t in a uniform register and reads the columns with
   // LDCU (uniform operand, no vector register); other spellings of the same loop made it
   // fall back to per-thread LDC + spills (tests/test_build_sass.py guards this).
-  // Double-buffered half-walk (Cols::kDoubleBuffer): the same steps, flips, products, signs and
-  // 16-term blocks as half_walk below, with step r writing the row sums into the other copy
-  // (r even: s -> s2, r odd: s2 -> s; four steps per iteration end in s).
-  // The opaque tz = t*zero in the loop-invariant row indices (as in half_walk) keeps ptxas from
-  // hoisting those rows' loads out of the loop into registers (which spilled).
-  template <class Cols>
-  __device__ __forceinline__ void half_walk_db(const Cols& cols, int T0, int H, int zero) {
-    double2 s2[N];
-    double mr = 0.0, mi = 0.0;
-    double orr = 0.0, oi = 0.0;
-    for (int t = -4; t < H - 4; t += 4) {
-      const int tz = t * zero;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const int b = (r == 0) ? ((__ffs(t + 4) - 1) & 15) : (__ffs(r) - 1);
-        const int d = (r == 0) ? (((T0 + t + 4) >> (b + 1)) & 1) : (r == 1) ? 0 : (r == 2) ? (((t + 4) >> 2) & 1) : 1;
-        const int row = (r == 0) ? (2 * b + d) : (2 * b + d + tz);
-        double2 p;
-        if ((r & 1) == 0) {
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            const double2 v = cols.get(row, i);
-            s2[i].x = __dadd_rn(s[i].x, v.x);
-            s2[i].y = __dadd_rn(s[i].y, v.y);
-          }
-          p = row_product<N>(s2);
-        } else {
-#pragma unroll
-          for (int i = 0; i < N; ++i) {
-            const double2 v = cols.get(row, i);
-            s[i].x = __dadd_rn(s2[i].x, v.x);
-            s[i].y = __dadd_rn(s2[i].y, v.y);
-          }
-          p = row_product<N>(s);
-        }
-        if (MODE == kSep) {
-          if (r & 1) { orr = __dadd_rn(orr, p.x); oi = __dadd_rn(oi, p.y); }
-          else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
-        } else if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
-        else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
-      }
-      if (((t + 4) & 12) == 12) {
-        if (MODE == kSep) { acc_add_sep(mr, mi, orr, oi); orr = 0.0; oi = 0.0; }
-        else acc_add(mr, mi);
-        mr = 0.0; mi = 0.0;
-      }
-    }
-    if (MODE == kSep) acc_add_sep(mr, mi, orr, oi);
-    else acc_add(mr, mi);
-  }
-
   // Row of the step-r = 0 flip into local index T0 + t + 4: Gray bit b = ctz(t + 4) (t = -4: bit
   // 15, an all-zero table row), direction bit b + 1 of the index.
   static __device__ __forceinline__ int head_row(int T0, int t) {
@@ -559,8 +511,7 @@ struct Walker {
     for (int h = 0; h < 2; ++h) {
       // direction = bit c of g = bit 0 of q: per-thread sign on the +u row (uniform index)
       if (h == 1) flip_signed(cols, plus_row(c - 1), (q & 1) ? kSgnDir1 : kSgnDir0);
-      if (Cols::kDoubleBuffer) half_walk_db(cols, h * H, H, zero);
-      else half_walk(cols, h * H, H, zero, u0);
+      half_walk(cols, h * H, H, zero, u0);
     }
   }
 
@@ -687,16 +638,46 @@ __device__ __forceinline__ void stage_transposed(const double2* __restrict__ A, 
 }
 
 // Canonical block reduction: contiguous pairwise tree over the block's threads (leaves),
-// node = left + right in double-double.  Result valid in red[0].
+// node = left + right in double-double: at level o (1, 2, 4, ...) thread t (a multiple of 2o)
+// adds the node of t + o.  Result valid in red[0] for thread 0 (blockDim a power of two).
+// Levels below 32 run inside each warp with shuffles (lane t takes lane t + o's node: the same
+// pairs, left + right, so the same bits as the shared-memory tree); the warp roots then go
+// through shared memory once and warp 0 finishes the levels above with shuffles -- one block
+// barrier instead of log2(blockDim) (m1_phases: the 7-level tree took ~2250 cycles per block).
+__device__ __forceinline__ Dd2 shfl_down_dd2(const Dd2& v, int o, unsigned mask) {
+  return Dd2{__shfl_down_sync(mask, v.re_hi, o), __shfl_down_sync(mask, v.re_lo, o),
+             __shfl_down_sync(mask, v.im_hi, o), __shfl_down_sync(mask, v.im_lo, o)};
+}
+
+// Levels o < width (a power of two <= 32) among the lanes in `mask` (every lane that executes).
+template <int MODE>
+__device__ __forceinline__ Dd2 warp_tree(Dd2 v, int lane, int width, unsigned mask) {
+  for (int o = 1; o < width; o <<= 1) {
+    const Dd2 u = shfl_down_dd2(v, o, mask);
+    if ((lane & (2 * o - 1)) == 0) v = part_add<MODE>(v, u);
+  }
+  return v;
+}
+
 template <int MODE = kComp>
 __device__ __forceinline__ void block_tree(Dd2* red, const Dd2& mine) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  PERM_CHECK(in_dyn_smem(red + tid, sizeof(Dd2)));
-  red[tid] = mine;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int nw = (nt + 31) >> 5;
+  // a block smaller than a warp has only its nt lanes
+  Dd2 v = warp_tree<MODE>(mine, lane, nt < 32 ? nt : 32, nt < 32 ? ((1u << nt) - 1u) : 0xffffffffu);
+  if (nw == 1) {
+    if (tid == 0) red[0] = v;
+    return;
+  }
+  PERM_CHECK(in_dyn_smem(red + warp, sizeof(Dd2)));
+  __syncthreads();                       // red may still be read by an earlier use
+  if (lane == 0) red[warp] = v;
   __syncthreads();
-  for (int o = 1; o < nt; o <<= 1) {
-    if ((tid & (2 * o - 1)) == 0 && tid + o < nt) red[tid] = part_add<MODE>(red[tid], red[tid + o]);
-    __syncthreads();
+  if (warp == 0) {
+    v = lane < nw ? red[lane] : Dd2{0.0, 0.0, 0.0, 0.0};
+    v = warp_tree<MODE>(v, lane, nw, 0xffffffffu);
+    if (lane == 0) red[0] = v;
   }
 }
 
@@ -752,12 +733,6 @@ __device__ __forceinline__ void build_tab(const double2* at, double2* tab, int c
 // launches (this + combine) instead of four.  The terms and their order are the sweep
 // kernel's (same table values, same flips, same accumulation), i.e. bit-identical results.
 constexpr int kSmallLog2 = 21;
-// Small single permanents walk with double-buffered row sums (SmemColumns DB) up to this n
-// (8n registers of row sums).
-#ifndef PERMB200_SMALL_DB
-#define PERMB200_SMALL_DB 1
-#endif
-__host__ __device__ constexpr bool small_double_buffer(int N) { return PERMB200_SMALL_DB && N <= 22; }
 
 template <int N, int ALG, int MODE>
 __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs args) {
@@ -770,7 +745,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_kernel(const SweepArgs 
   __syncthreads();
   build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
   __syncthreads();
-  const SmemColumns<N, small_double_buffer(N)> cols{tab};
+  const SmemColumns<N> cols{tab};
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   const int ubits = args.block_bits + args.lam + args.c;
@@ -852,7 +827,7 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
   build_tab<N, ALG>(at, tab, args.c < kCMax ? args.c : kCMax);
   __syncthreads();
   PERM_PHASE(2, ph_t);
-  const SmemColumns<N, small_double_buffer(N)> cols{tab};
+  const SmemColumns<N> cols{tab};
   const uint64_t unit = (uint64_t)(args.unit_lo + blockIdx.x);
   const uint64_t leaf_id = (unit << args.block_bits) + threadIdx.x;
   Dd2 mine;
@@ -893,9 +868,6 @@ __global__ void __launch_bounds__(kMaxBlock) sweep_small_fused_kernel(const Swee
 // blocks/SM, 9.2 waves for M2's 4096 permanents; ncu profiles/r01_batched_m2_*) leaves warps
 // idle.  At 4 blocks (<= 128 registers) chunk_fast<16> still has no spills (only the kernel
 // body spills a few values across the chunk call).
-#ifndef PERMB200_BATCHED_DB           // A/B: double-buffered row sums in the batched walk
-#define PERMB200_BATCHED_DB false
-#endif
 #ifdef PERMB200_BATCHED_MINB          // A/B experiments (tools/microbench/batched_bench.cu)
 __host__ __device__ constexpr int batched_min_blocks(int N) { return N <= 16 ? PERMB200_BATCHED_MINB : N <= 20 ? 3 : 1; }
 #else
@@ -925,7 +897,7 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
       tab[k] = v;
     }
     __syncthreads();
-    const SmemColumns<N, PERMB200_BATCHED_DB> cols{tab};
+    const SmemColumns<N> cols{tab};
     const uint64_t terms = 1ull << (N - 1);
     Dd2 mine;
     if (args.c >= kMinFastC) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);

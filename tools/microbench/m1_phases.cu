@@ -3,7 +3,7 @@
 // when built with -DPERMB200_PHASE_TIMES -- its phases (staging, column table, walk, block tree,
 // grid barrier, final reduce) from %globaltimer / clock64 stamps.  A/B of compile-time shapes:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Iinclude \
-//        -Ipaper_1606_05836_b200/csrc [-DPERMB200_PHASE_TIMES] [-DPERMB200_SMALL_DB=0] \
+//        -Ipaper_1606_05836_b200/csrc [-DPERMB200_PHASE_TIMES] [-DPERMB200_SMALL_BUILD=0] \
 //        tools/microbench/m1_phases.cu -o tools/microbench/m1_phases_X
 #include <cstdio>
 #include <cstdlib>
