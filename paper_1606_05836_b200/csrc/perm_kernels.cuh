@@ -193,8 +193,12 @@ __host__ __device__ constexpr bool acc_in_smem(int N) { return N <= 51 || N == 5
 #ifndef PERMB200_SMALL_BUILD          // A/B switch (tools/microbench/m1_phases.cu)
 #define PERMB200_SMALL_BUILD 1
 #endif
-__host__ __device__ constexpr int build_rows(int N) { return (PERMB200_SMALL_BUILD && N <= 24) ? N : 8; }
-__host__ __device__ constexpr int build_col_unroll(int N) { return (PERMB200_SMALL_BUILD && N <= 24) ? 2 : 1; }
+// WIDE: the column source's kernel has registers to spare (not the batched kernel, which is
+// capped at 128 registers for 4 blocks/SM and spilled with the wide build).
+__host__ __device__ constexpr int build_rows(int N, bool WIDE) { return (PERMB200_SMALL_BUILD && WIDE && N <= 24) ? N : 8; }
+__host__ __device__ constexpr int build_col_unroll(int N, bool WIDE) {
+  return (PERMB200_SMALL_BUILD && WIDE && N <= 24) ? 2 : 1;
+}
 
 #ifndef PERMB200_N50_CHAINS            // A/B switch for the M5 size (tools/microbench/sweep_bench.cu)
 #define PERMB200_N50_CHAINS 4
@@ -248,6 +252,7 @@ __host__ __device__ constexpr bool row_ahead(int N) {
 
 struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
+  static constexpr bool kWideBuild = true;    // Walker::build: all rows per pass for n <= 24
   static constexpr bool kBit0Cached = false;  // uniform LDCU operands cost no vector registers
   int base;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -259,11 +264,12 @@ struct ConstColumns {
 
 // SmemColumns: a per-block shared-memory table with the same layout as the constant one:
 // tab[(2b+d)*N + i] = signed step vector of Gray bit b, direction d (zero rows for b >= c).
-template <int N>
+template <int N, bool WIDE = true>
 struct SmemColumns {
   // The batched kernel reads its columns from shared memory; with shared-memory accumulators
   // too (and their layout) M2 measured 28 % slower (1.11 vs 0.865 ms): registers there.
   static constexpr bool kSmemAccOk = false;
+  static constexpr bool kWideBuild = WIDE;
   static constexpr bool kBit0Cached = PERMB200_BIT0_CACHE;
   const double2* tab;
   __device__ __forceinline__ double2 get(int row, int i) const {
@@ -374,8 +380,9 @@ struct Walker {
   // share of a chunk (M1: 32-term chunks) and was bound by the shared-memory load latency of
   // each 8-row column slice (m1_phases: ~6000 of the walk's 15500 cycles per block).  Every row
   // sum is accumulated over the same columns in the same order: the same bits either way.
+  template <bool WIDE = false>
   __device__ __forceinline__ void build(const double2* __restrict__ at, uint64_t G) {
-    constexpr int RB = build_rows(N);
+    constexpr int RB = build_rows(N, WIDE);
 #pragma unroll
     for (int r0 = 0; r0 < N; r0 += RB) {
 #pragma unroll
@@ -384,7 +391,7 @@ struct Walker {
           if (ALG == kGlynn) s[i] = make_double2(0.5 * at[i].x, 0.5 * at[i].y);  // delta_1 = +1; exact
           else s[i] = make_double2(0.0, 0.0);          // Ryser: S starts empty
         }
-#pragma unroll (build_col_unroll(N))
+#pragma unroll (build_col_unroll(N, WIDE))
       for (int j = (ALG == kGlynn) ? 1 : 0; j < N; ++j) {
         const int bit = (ALG == kGlynn) ? (int)((G >> (j - 1)) & 1) : (int)((G >> j) & 1);
         // at holds kScale * a: weight delta_j / 2 (Glynn) reproduces RN(s + delta_j a_ij) exactly
@@ -498,7 +505,7 @@ struct Walker {
   template <class Cols>
   __device__ __forceinline__ void fast_chunk(const Cols& cols, const double2* __restrict__ at, uint64_t q, int c, int zero) {
     const uint64_t g0 = q << c;
-    build(at, g0 ^ (g0 >> 1));
+    build<Cols::kWideBuild>(at, g0 ^ (g0 >> 1));
     const int H = 1 << (c - 1);
     double2 u0[N];                  // Cols::kBit0Cached: table row 0 (bit 0, direction 0)
     if (Cols::kBit0Cached) {
@@ -897,7 +904,7 @@ __global__ void __launch_bounds__(kMaxBlock, batched_min_blocks(N)) batched_kern
       tab[k] = v;
     }
     __syncthreads();
-    const SmemColumns<N> cols{tab};
+    const SmemColumns<N, false> cols{tab};
     const uint64_t terms = 1ull << (N - 1);
     Dd2 mine;
     if (args.c >= kMinFastC) mine = walk_leaf<N, kGlynn, true, false>(cols, at, threadIdx.x, args.c, args.lam, 0, terms, args.zero);
