@@ -95,8 +95,10 @@ enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_R
  *   chunk      = 2^chunk_bits consecutive Gray indices walked by one leaf from a fresh
  *                O(n^2) row-sum build (the drift reset)
  *   leaf       = 2^leaf_bits chunks, walked in order by one group of `lanes` threads into one
- *                dd accumulator; lanes = 1, or 4 (small n: m <= 21, n >= 8) / 2 (n >= 52,
- *                compensated mode) with the n row sums split over the lanes
+ *                dd partial; lanes = 1, or 2 (n >= 52, compensated mode) with the n row sums
+ *                split over the two: lane l of a PAIR OF WARPS (rows [0, ceil(n/2)) in the
+ *                even warp, the rest in the odd one; the plan's block_bits is 6) -- or two
+ *                adjacent lanes of one warp for custom plans with block_bits < 5
  *   unit       = 2^block_bits leaves (one thread block of 2^block_bits * lanes threads) -> one
  *                dd partial
  *   units      = 2^unit_bits; unit_terms = terms / units */
@@ -110,8 +112,9 @@ typedef struct {
 
 /* Largest supported n (64 for Glynn; Ryser stops at 63 because its 2^n Gray indices
  * must fit in uint64).  The FP64 sweep keeps every row sum in registers for all n: one thread
- * per chunk (4n registers) up to n = 51, two lanes per chunk (2n registers each) from 52 on
- * (the plain and separate-addition modes keep one thread per chunk there and spill). */
+ * per chunk (4n registers) up to n = 51, two threads per chunk (2n registers each, one per
+ * warp of a warp pair) from 52 on (the plain and separate-addition modes keep one thread per
+ * chunk there and spill). */
 int perm_max_n(void);
 
 /* Human-readable text for a status code (for PERM_ECUDA: the last CUDA error seen by

@@ -12,6 +12,7 @@
 
 #include "../../include/permb200.h"
 #include "perm_registry.h"
+#include "perm_kernels_wsplit.cuh"   // wsplit_launches
 
 using namespace permb200;
 
@@ -86,7 +87,8 @@ constexpr int kAlgs = 8;
 SweepLauncher g_sweep[kAlgs][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, RYSER_DD, GLYNN_PLAIN, RYSER_PLAIN, GLYNN_SEP, RYSER_SEP
 SweepLauncher g_small[kAlgs][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
 FusedLauncher g_small_fused[kAlgs][kNMax + 1];   // the same + grid barrier + combine, one launch
-SweepLauncher g_split[kAlgs][kNMax + 1];   // row-split sweep (perm_kernels_split.cuh): n >= 52
+SweepLauncher g_split[kAlgs][kNMax + 1];   // 2-lane row split (perm_kernels_split.cuh): fallback
+SweepLauncher g_wsplit[kAlgs][kNMax + 1];  // warp-pair row split (perm_kernels_wsplit.cuh): n >= 52
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {
@@ -118,6 +120,8 @@ void init_tables() {
     register_small(g_small);
     register_small_fused(g_small_fused);
     register_split_large(g_split);
+    register_wsplit_a(g_wsplit);
+    register_wsplit_b(g_wsplit);
     register_batched_a(g_batched);
     register_batched_b(g_batched);
   });
@@ -142,8 +146,10 @@ int mode_of(int alg) { return is_plain(alg) ? kPlain : is_sep(alg) ? kSep : kCom
 int sep_sign(int n, int alg) { return !is_sep(alg) ? 0 : (!is_glynn(alg) && (n & 1)) ? -1 : 1; }
 
 // Lanes per chunk (leaf) of the FP64 sweep: 2 for n >= kSplitLargeN in the compensated mode (4n
-// row-sum registers do not fit one thread), else 1 (perm_kernels_split.cuh).  Small n (m <=
-// kSmallLog2) walks one thread per chunk with double-buffered row sums (SmemColumns DB): the
+// row-sum registers do not fit one thread), else 1.  Two lanes = the same lane of a warp pair
+// (perm_kernels_wsplit.cuh: constant-bank columns, half products exchanged through shared
+// memory), or -- custom plans with block_bits < 5 -- two adjacent lanes of one warp
+// (perm_kernels_split.cuh).  Small n (m <= kSmallLog2) walks one thread per chunk: the
 // 4-lane split measured slower on M1 (n = 20: 26.7 / 47.2 us per Glynn / Ryser call against
 // 18.5 / 22.6 us for one lane, profiles/r02_m1_latency_split4.log) -- at ~1 warp per scheduler the
 // FP64 pipe, not the per-thread chain, bounds it, and the split adds shuffles and a combine cmul.
@@ -301,8 +307,10 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   a.unit_lo = u_lo;
   a.c = P.chunk_bits; a.lam = P.leaf_bits; a.block_bits = P.block_bits;
   a.zero = 0;
-  if (P.lanes > 1 && g_split[P.alg][P.n]) {
-    // row-split sweep: columns from shared memory, capturable, no constant slot
+  const bool wsplit = P.lanes > 1 && g_wsplit[P.alg][P.n] && P.block_bits >= 5 && P.block_bits <= 6;
+  if (P.lanes > 1 && !wsplit && g_split[P.alg][P.n]) {
+    // 2-lane row split (plans with fewer than 32 leaves per unit): columns from shared memory,
+    // capturable, no constant slot
     a.slot = 0; a.col_base = 0;
     CUDA_TRY(g_split[P.alg][P.n](a, u_hi - u_lo, staging, st), "split sweep launch");
     note_launch();
@@ -344,8 +352,14 @@ int run_sweep(const perm_c128* A, const perm_plan_t& P, int64_t u_lo, int64_t u_
   if (ds.used[slot]) CUDA_TRY(cudaStreamWaitEvent(st, ds.ev[slot], 0), "cudaStreamWaitEvent");
   a.slot = slot;
   a.col_base = slot * kTabRows * kNMax;
-  CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "sweep launch");
-  note_launch(a.c >= kMinFastC ? 2 : 1);   // column staging (fast path) + sweep
+  if (wsplit) {
+    // warp-pair row split: constant-bank columns like the one-lane sweep (+ ragged end units)
+    CUDA_TRY(g_wsplit[P.alg][P.n](a, u_hi - u_lo, staging, st), "warp-split sweep launch");
+    note_launch(wsplit_launches(a, u_hi - u_lo));
+  } else {
+    CUDA_TRY(g_sweep[P.alg][P.n](a, u_hi - u_lo, staging, st), "sweep launch");
+    note_launch(a.c >= kMinFastC ? 2 : 1);   // column staging (fast path) + sweep
+  }
   CUDA_TRY(cudaEventRecord(ds.ev[slot], st), "cudaEventRecord");
   ds.used[slot] = true;
   return PERM_OK;

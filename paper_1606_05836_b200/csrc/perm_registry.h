@@ -30,6 +30,8 @@ void register_sep_ryser_b(SweepLauncher* t);
 void register_small(SweepLauncher (*t)[kNMax + 1]);
 void register_small_fused(FusedLauncher (*t)[kNMax + 1]);
 void register_split_large(SweepLauncher (*t)[kNMax + 1]);
+void register_wsplit_a(SweepLauncher (*t)[kNMax + 1]);
+void register_wsplit_b(SweepLauncher (*t)[kNMax + 1]);
 void register_batched_a(BatchedLauncher* t);
 void register_batched_b(BatchedLauncher* t);
 }  // namespace permb200
