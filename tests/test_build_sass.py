@@ -62,3 +62,26 @@ def test_hot_loop_has_no_spills_up_to_n51(obj, n, alg):
     assert spills == 0, (n, spills)
     assert c["IMAD.MOV.U32"] + c["MOV"] <= 16, (n, c["IMAD.MOV.U32"] + c["MOV"])
     assert c["DADD"] + c["DMUL"] + c["DFMA"] > 0
+
+
+def _function(sass, want):
+    for f in re.split(r"\n\s*Function : ", sass):
+        if want in f.split("\n")[0]:
+            return f
+    raise AssertionError(f"{want} not found")
+
+
+@pytest.mark.parametrize("obj,n,alg", [("perm_inst_wsplit_a.o", 52, 0), ("perm_inst_wsplit_a.o", 53, 1),
+                                       ("perm_inst_wsplit_a.o", 54, 0), ("perm_inst_wsplit_b.o", 56, 0),
+                                       ("perm_inst_wsplit_b.o", 63, 1), ("perm_inst_wsplit_b.o", 64, 0)])
+def test_wsplit_columns_uniform_and_no_spills(obj, n, alg):
+    """The warp-pair row split (perm_kernels_wsplit.cuh, n >= 52): the warp index reaches the
+    K-branches through a shuffle so ptxas sees them as warp-uniform -- the columns must stay
+    LDCU uniform operands (the plain (threadIdx.x >> 5) & 1 spelling fell back to per-thread LDC
+    for every column) -- and the whole kernel (both half-walk copies) has no local memory."""
+    f = _function(_sass(obj), f"wsplit_kernelILi{n}ELi{alg}ELi0E")
+    ldcu = len(re.findall(r"\bLDCU", f))
+    ldc_vec = len(re.findall(r"LDC(?:\.64)? R\d+, c\[0x3\]\[R", f))
+    assert ldcu >= 10 * n and ldc_vec == 0, (ldcu, ldc_vec)
+    assert not re.search(r"\b(STL|LDL)", f)
+    assert "BAR.SYNC" in f or "BAR.SYNC.DEFER_BLOCKING" in f or "BAR " in f
