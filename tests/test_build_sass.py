@@ -73,7 +73,7 @@ def _function(sass, want):
 
 @pytest.mark.parametrize("obj,n,alg", [("perm_inst_wsplit_a.o", 52, 0), ("perm_inst_wsplit_a.o", 53, 1),
                                        ("perm_inst_wsplit_a.o", 54, 0), ("perm_inst_wsplit_b.o", 56, 0),
-                                       ("perm_inst_wsplit_b.o", 63, 1), ("perm_inst_wsplit_b.o", 64, 0)])
+                                       ("perm_inst_wsplit_b.o", 59, 1), ("perm_inst_wsplit_b.o", 60, 0)])
 def test_wsplit_columns_uniform_and_no_spills(obj, n, alg):
     """The warp-pair row split (perm_kernels_wsplit.cuh, n >= 52): the warp index reaches the
     K-branches through a shuffle so ptxas sees them as warp-uniform -- the columns must stay

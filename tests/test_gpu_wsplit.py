@@ -1,5 +1,5 @@
 """The warp-pair row-split sweep (paper_1606_05836_b200/csrc/perm_kernels_wsplit.cuh), the FP64
-sweep of the canonical plan from n = 52 (Eq. (2), Eq. (1); SURVEY §8 a3/a4 "row
+sweep of the canonical plan for n = 52..60 (n = 61..64: the 2-lane split of one warp, same plan; Eq. (2), Eq. (1); SURVEY §8 a3/a4 "row
 sums kept in registers for n <= 64"): each chunk's row sums live in lane l of a PAIR of warps and
 the two half products meet through shared memory.
 
@@ -34,8 +34,8 @@ def _c(d):
     return complex(d[0] + d[1], d[2] + d[3])
 
 
-@pytest.mark.parametrize("n,alg", [(52, "glynn"), (53, "glynn"), (53, "ryser"), (58, "glynn"), (63, "ryser"),
-                                   (64, "glynn")])
+@pytest.mark.parametrize("n,alg", [(52, "glynn"), (53, "glynn"), (53, "ryser"), (58, "glynn"), (59, "ryser"),
+                                   (60, "glynn"), (63, "ryser"), (64, "glynn")])
 def test_wsplit_fast_units_vs_oracle(n, alg):
     A = synth.gaussian(n, 9700 + n)
     dA = T(A)
@@ -57,13 +57,13 @@ def test_wsplit_fast_units_vs_oracle(n, alg):
 def test_wsplit_unit_partials_independent_of_launch():
     n = 55
     A = T(synth.gaussian(n, 4455))
-    c, wb = 5, 6
-    whole = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, 0, wb, 100, 164).cpu().numpy()
+    c, lam, wb = 5, 3, 6                  # 2^(54 - 14) = 2^40 units: the custom-plan API's maximum
+    whole = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, lam, wb, 100, 164).cpu().numpy()
     for lo, hi in ((100, 101), (131, 164), (150, 151)):
-        part = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, 0, wb, lo, hi).cpu().numpy()
+        part = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, lam, wb, lo, hi).cpu().numpy()
         assert np.array_equal(part, whole[lo - 100:hi - 100]), (lo, hi)
     # repeated launches: deterministic
-    again = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, 0, wb, 100, 164).cpu().numpy()
+    again = pb.sweep_units_custom(A, pb.ALG_GLYNN, c, lam, wb, 100, 164).cpu().numpy()
     assert np.array_equal(again, whole)
 
 
