@@ -350,6 +350,19 @@ def run_ours(args, rank, world, local_rank, shared_gpu: bool):
                                     "source": "profiles/r01_m5_full.json (tools/m5_run.py)"}
         except (ValueError, KeyError, OSError):
             pass
+    # The Glynn-Ryser discrepancy toward n = 50 (BASELINE.json config 5): full FP64 Glynn and
+    # Ryser permanents of the M5 family measured at n = 40..48 (tools/r02/ladder_summary.py);
+    # the n = 50 figure is a band fitted to those rungs, labelled as such.
+    lad = os.path.join(ROOT, "profiles", "r02_discrepancy_ladder.json")
+    if os.path.exists(lad):
+        try:
+            r = json.load(open(lad))
+            line["glynn_ryser_discrepancy"] = {
+                "measured": {str(x["n"]): x["glynn_ryser_rel_discrepancy"] for x in r["rungs"]},
+                "n50_fitted_band_1sigma": (r.get("extrapolation_n50") or {}).get("n50_band_1sigma"),
+                "source": "profiles/r02_discrepancy_ladder.json (measured rungs; n = 50 is a fit, not a run)"}
+        except (ValueError, KeyError, OSError):
+            pass
     print(json.dumps(line), flush=True)
     return 0
 

@@ -249,6 +249,14 @@ __host__ __device__ constexpr bool row_ahead(int N) {
 #ifndef PERMB200_BIT0_CACHE
 #define PERMB200_BIT0_CACHE 0
 #endif
+// Terms per half-walk loop iteration: 4 (bit-0 flips with compile-time directions), or 2 for
+// N >= PERMB200_UNROLL2_FROM (half the loop body: the n = 50 body of 4 terms is ~30 KB of SASS
+// against a 32 KB L1.5 instruction cache; the bit-0 direction becomes a loop-carried uniform
+// value).  Same flips, same terms, same accumulation order: bit-identical results.
+#ifndef PERMB200_UNROLL2_FROM          // A/B switch (tools/microbench/sweep_bench.cu)
+#define PERMB200_UNROLL2_FROM 999
+#endif
+__host__ __device__ constexpr bool walk_unroll2(int N) { return N >= PERMB200_UNROLL2_FROM; }
 
 struct ConstColumns {
   static constexpr bool kSmemAccOk = true;    // see Walker::kSmemAcc
@@ -464,6 +472,29 @@ struct Walker {
     // Per n (spill-free SASS only, tools/sass_loop_stats.py: on for n <= 46 and n = 49; at n = 48,
     // 50, 51 the extra live value tipped ptxas into spills).
     constexpr bool kAhead = row_ahead(N);
+    if constexpr (walk_unroll2(N) && MODE != kSep && !Cols::kBit0Cached) {
+      // 2 terms per iteration: local indices T0+t+2 (Gray bit ctz(t+2); t = -2: the all-zero
+      // row of bit 15) and T0+t+3 (bit 0, direction = bit 1 of the index).
+      for (int t = -2; t < H - 2; t += 2) {
+        const int tz = t * zero;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int b = (r == 0) ? ((__ffs(t + 2) - 1) & 15) : 0;
+          const int d = (r == 0) ? (((T0 + t + 2) >> (b + 1)) & 1) : (((t + 2) >> 1) & 1);
+          const int row = (r == 0) ? (2 * b + d) : (d + tz);
+          flip_row(cols, row);
+          const double2 p = row_product<N>(s);
+          if (((r & 1) != 0) != kNegBase) { mr = __dsub_rn(mr, p.x); mi = __dsub_rn(mi, p.y); }
+          else { mr = __dadd_rn(mr, p.x); mi = __dadd_rn(mi, p.y); }
+        }
+        if (((t + 2) & 14) == 14) {
+          acc_add(mr, mi);
+          mr = 0.0; mi = 0.0;
+        }
+      }
+      acc_add(mr, mi);
+      return;
+    }
     int row0_next = head_row(T0, -4);
     for (int t = -4; t < H - 4; t += 4) {
       const int tz = t * zero;

@@ -30,6 +30,10 @@
 
 namespace permb200 {
 
+#ifndef PERMB200_WSPLIT_U2             // A/B switch (tools/microbench/wsplit_bench.cu)
+#define PERMB200_WSPLIT_U2 0
+#endif
+
 __device__ __forceinline__ void pair_barrier(int id) {
   asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory");
 }
@@ -131,6 +135,39 @@ struct HalfWalker {
                                             int lane) {
     double mr = 0.0, mi = 0.0;
     int slot = 0;
+#if PERMB200_WSPLIT_U2
+    // A/B variant: 2 terms per exchange (half the loop body; the two warps of a pair run
+    // different bodies, together > 32 KB of SASS from n = 50 with 4 terms).  The lower warp
+    // finishes the even terms, the upper warp the odd ones; one barrier per 2 terms.
+    for (int t = -2; t < H - 2; t += 2) {
+      const int tz = t * zero;
+      double2 keep = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int b = (r == 0) ? ((__ffs(t + 2) - 1) & 15) : 0;
+        const int d = (r == 0) ? (((T0 + t + 2) >> (b + 1)) & 1) : (((t + 2) >> 1) & 1);
+        const int row = (r == 0) ? (2 * b + d) : (d + tz);
+        flip_row(cols, row);
+        const double2 p = half_product();
+        if (r == K) keep = p;
+        else xb[((slot * 2 + K) * 2) * 32 + lane] = p;
+      }
+      pair_barrier(bar);
+      {
+        const double2 o = xb[((slot * 2 + (1 - K)) * 2) * 32 + lane];
+        const double2 term = (K == 0) ? cmul(keep, o) : cmul(o, keep);    // cmul(lower, upper)
+        if ((K != 0) != kNegBase) { mr = __dsub_rn(mr, term.x); mi = __dsub_rn(mi, term.y); }
+        else { mr = __dadd_rn(mr, term.x); mi = __dadd_rn(mi, term.y); }
+      }
+      slot ^= 1;
+      if (((t + 2) & 14) == 14) {
+        acc_add(mr, mi);
+        mr = 0.0; mi = 0.0;
+      }
+    }
+    acc_add(mr, mi);
+    return;
+#endif
     for (int t = -4; t < H - 4; t += 4) {
       const int tz = t * zero;
       double2 keep0 = make_double2(0.0, 0.0), keep1 = make_double2(0.0, 0.0);

@@ -59,7 +59,12 @@ int main(int argc, char** argv) {
   const int waves = argc > 1 ? atoi(argv[1]) : 8;
   run<32, kGlynn>(waves);
   run<40, kGlynn>(waves);
+  run<44, kGlynn>(waves);
+  run<46, kGlynn>(waves);
+  run<48, kGlynn>(waves);
+  run<49, kGlynn>(waves);
   run<50, kGlynn>(waves);
+  run<51, kGlynn>(waves);
   run<50, kRyser>(waves);
   return 0;
 }
