@@ -97,9 +97,8 @@ enum { PERM_ALG_GLYNN = 0, PERM_ALG_RYSER = 1, PERM_ALG_GLYNN_DD = 2, PERM_ALG_R
  *   leaf       = 2^leaf_bits chunks, walked in order by one group of `lanes` threads into one
  *                dd partial; lanes = 1, or 2 (n >= 52, compensated mode) with the n row sums
  *                split over the two: lane l of a PAIR OF WARPS (rows [0, ceil(n/2)) in the
- *                even warp, the rest in the odd one; the plan's block_bits is 6) for
- *                n = 52..60 -- or two adjacent lanes of one warp for n = 61..64 (measured
- *                faster there) and for custom plans with block_bits < 5
+ *                even warp, the rest in the odd one; the plan's block_bits is 6) -- or two
+ *                adjacent lanes of one warp for custom plans with block_bits < 5
  *   unit       = 2^block_bits leaves (one thread block of 2^block_bits * lanes threads) -> one
  *                dd partial
  *   units      = 2^unit_bits; unit_terms = terms / units */
@@ -113,8 +112,8 @@ typedef struct {
 
 /* Largest supported n (64 for Glynn; Ryser stops at 63 because its 2^n Gray indices
  * must fit in uint64).  The FP64 sweep keeps every row sum in registers for all n: one thread
- * per chunk (4n registers) up to n = 51, two threads per chunk (2n registers each: one per
- * warp of a warp pair for n = 52..60, two adjacent lanes for n = 61..64) from 52 on (the plain and separate-addition modes keep one thread per
+ * per chunk (4n registers) up to n = 51, two threads per chunk (2n registers each, one per
+ * warp of a warp pair) from 52 on (the plain and separate-addition modes keep one thread per
  * chunk there and spill). */
 int perm_max_n(void);
 

@@ -88,7 +88,7 @@ SweepLauncher g_sweep[kAlgs][kNMax + 1];   // [alg][n]: GLYNN, RYSER, GLYNN_DD, 
 SweepLauncher g_small[kAlgs][kNMax + 1];   // small-n shared-memory-column sweep (m <= kSmallLog2)
 FusedLauncher g_small_fused[kAlgs][kNMax + 1];   // the same + grid barrier + combine, one launch
 SweepLauncher g_split[kAlgs][kNMax + 1];   // 2-lane row split (perm_kernels_split.cuh): fallback
-SweepLauncher g_wsplit[kAlgs][kNMax + 1];  // warp-pair row split (perm_kernels_wsplit.cuh): n = 52..60
+SweepLauncher g_wsplit[kAlgs][kNMax + 1];  // warp-pair row split (perm_kernels_wsplit.cuh): n >= 52
 BatchedLauncher g_batched[kNMax + 1];
 
 void init_tables() {

@@ -1,5 +1,5 @@
 """The warp-pair row-split sweep (paper_1606_05836_b200/csrc/perm_kernels_wsplit.cuh), the FP64
-sweep of the canonical plan for n = 52..60 (n = 61..64: the 2-lane split of one warp, same plan; Eq. (2), Eq. (1); SURVEY §8 a3/a4 "row
+sweep of the canonical plan from n = 52 (4 terms per exchange up to n = 59, 2 from n = 60; Eq. (2), Eq. (1); SURVEY §8 a3/a4 "row
 sums kept in registers for n <= 64"): each chunk's row sums live in lane l of a PAIR of warps and
 the two half products meet through shared memory.
 
