@@ -12,12 +12,17 @@ PRE=${2:-}
 mkdir -p gpurun_out/ladder
 if [ -n "$PRE" ]; then bash -c "$PRE"; fi
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu --format=csv >> gpurun_out/ladder/smi.txt 2>&1
-for job in "46 glynn" "46 ryser" "48 glynn" "48 ryser"; do
+# LADDER_JOBS="41 glynn;41 ryser;..." overrides the job list (';'-separated "<n> <alg>" pairs)
+IFS=';' read -ra JOBS <<< "${LADDER_JOBS:-46 glynn;46 ryser;48 glynn;48 ryser}"
+for job in "${JOBS[@]}"; do
   set -- $job
   N=$1; ALG=$2; J=g${N}_${ALG}
   if [ -f runs/ladder/$J/COMPLETE ]; then continue; fi
   BUDGET=$(( TOTAL - ($(date +%s) - T0) - 240 ))
   [ $BUDGET -lt 90 ] && break
+  # a job that cannot finish in what is left is skipped, not started (LADDER_NEED_<job> seconds)
+  NEED_VAR=LADDER_NEED_${J}; NEED=${!NEED_VAR:-0}
+  if [ $BUDGET -lt $NEED ]; then echo "$J skipped: budget $BUDGET < need $NEED" >> gpurun_out/ladder/session.log; continue; fi
   mkdir -p gpurun_out/ladder/$J runs/ladder/$J
   echo "$J start $(date) budget_s=$BUDGET" >> gpurun_out/ladder/session.log
   python tools/m5_run.py --workload gauss50:$N --alg $ALG --ledger-in runs/ladder/$J --out gpurun_out/ladder/$J \

@@ -35,7 +35,7 @@ def job(n, alg):
         "segments": len({int(r["segment"]) for r in rows}), "segments_total": st.get("segments_total"),
         "sessions": len({r.get("session") for r in rows}),
         "device_seconds": dev_s, "terms": terms, "terms_per_s": terms / dev_s if dev_s else None,
-        "fp64_issue_frac_nominal": terms / dev_s * (6 * n - 2) / (148 * 64 * 1.965e9) if dev_s else None,
+        "fp64_issue_frac_nominal": terms / dev_s * (6 * n - 2) / (148 * 64 * 1.965e9) if dev_s and not alg.endswith("_dd") else None,
         "sm_mhz_min": min(sm) if sm else None, "sm_mhz_median": statistics.median(sm) if sm else None,
         "throttle_reasons": sorted({x for r in rows for x in (r.get("reasons") or "").split("|") if x}),
     }
@@ -47,14 +47,27 @@ for r in r01["rows"]:
     rungs.append({"n": r["n"], "glynn_ryser_rel_discrepancy": r["glynn_ryser_rel_discrepancy"],
                   "source": a.r01, "glynn": r["glynn"], "ryser": r["ryser"]})
 new = {}
-for n in (46, 48):
+import re
+sizes = sorted({int(m.group(1)) for d in glob.glob(os.path.join(a.runs, "g*_*"))
+                for m in [re.match(r"g(\d+)_", os.path.basename(d))] if m})
+for n in sizes:
     g, r = job(n, "glynn"), job(n, "ryser")
     new[n] = {"glynn": g, "ryser": r}
+    rung = None
     if g["complete"] and r["complete"]:
         G = complex(*g["value"])
         R = complex(*r["value"])
-        rungs.append({"n": n, "glynn_ryser_rel_discrepancy": abs(G - R) / abs(G), "source": f"{a.runs}/g{n}_*",
-                      "glynn": g["value"], "ryser": r["value"]})
+        rung = {"n": n, "glynn_ryser_rel_discrepancy": abs(G - R) / abs(G), "source": f"{a.runs}/g{n}_*",
+                "glynn": g["value"], "ryser": r["value"]}
+        rungs.append(rung)
+    if os.path.isdir(os.path.join(a.runs, f"g{n}_glynn_dd")):
+        d = job(n, "glynn_dd")
+        new[n]["glynn_dd"] = d
+        if rung and d["complete"]:
+            D = complex(*d["value"])
+            rung["glynn_dd"] = d["value"]
+            rung["rel_err_glynn_vs_dd"] = abs(complex(*g["value"]) - D) / abs(D)
+            rung["rel_err_ryser_vs_dd"] = abs(complex(*r["value"]) - D) / abs(D)
 rungs.sort(key=lambda x: x["n"])
 # The discrepancy is Ryser's rounding error over |perm|, and |perm| of one Gaussian realisation
 # fluctuates by an order of magnitude around its e^(-n/2)-like trend, so the rungs are not
