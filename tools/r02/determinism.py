@@ -30,6 +30,7 @@ def T(x):
 
 
 A20, A24, A52 = T(synth.gaussian(20, 1)), T(synth.gaussian(24, 2)), T(synth.gaussian(52, 3))
+A60 = T(synth.gaussian(60, 4))
 As = T(synth.haar_batch(512, 256, 16, 16, 17))
 cases = {
     "fused split n=20 glynn": lambda s: pb.glynn(A20),
@@ -40,6 +41,10 @@ cases = {
     "sep n=20": lambda s: pb.perm_alg(A20, "glynn_sep"),
     "batched n=16": lambda s: pb.glynn_batched(As),
     "2-lane split n=52 range": lambda s: pb.glynn_range(A52, 777, 777 + (1 << 15)),
+    # warp-pair split (perm_kernels_wsplit.cuh): shared-memory exchange + named barriers;
+    # n = 52: 4 terms per exchange, n = 60: 2 terms per exchange
+    "warp-pair n=52 units": lambda s: pb.sweep_units_custom(A52, "glynn", 5, 0, 6, 1000, 1296),
+    "warp-pair n=60 units": lambda s: pb.sweep_units_custom(A60, "ryser", 6, 8, 6, 1000, 1296),
 }
 streams = [torch.cuda.Stream(dev) for _ in range(4)]
 bad = 0
