@@ -45,7 +45,8 @@ rungs = []
 r01 = json.load(open(a.r01))
 for r in r01["rows"]:
     rungs.append({"n": r["n"], "glynn_ryser_rel_discrepancy": r["glynn_ryser_rel_discrepancy"],
-                  "source": a.r01, "glynn": r["glynn"], "ryser": r["ryser"]})
+                  "source": a.r01, "glynn": r["glynn"], "ryser": r["ryser"],
+                  **{k: r[k] for k in ("rel_err_glynn_vs_dd", "rel_err_ryser_vs_dd") if k in r}})
 new = {}
 import re
 sizes = sorted({int(m.group(1)) for d in glob.glob(os.path.join(a.runs, "g*_*"))
